@@ -1,0 +1,98 @@
+// kernels.h -- host-side launchers implemented in the .cu files and used by
+// the C-ABI layer (api.cpp).  Internal; not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace fse {
+
+// ---------------------------------------------------------------- generic
+struct GenArgs {
+  int count, M, N, iterations, precision;  // precision: 0 f64, 1 f32
+  double rho, gamma;
+  const double *signal;
+  const int8_t *labels;
+  long long labels_stride;
+  const int32_t *label_index;  // optional: window i uses labels + label_index[i]*labels_stride
+  double *recon, *model;
+  int64_t *us, *vs;
+  double *cs, *es;
+  int32_t *status;
+};
+// Size of the global workspace the generic extrapolation needs for `count`
+// windows (0 when everything fits in shared memory).
+size_t generic_workspace_bytes(int count, int M, int N, int precision);
+cudaError_t launch_generic_extrapolate(const GenArgs &a, void *workspace, cudaStream_t s);
+
+cudaError_t launch_cfse_kernel_f64(int count, int M, int N, double *R, const double *W,
+                                   long long w_stride, double gamma, const double *inv_w00,
+                                   int iterations, const double *e0, double *G, int64_t *us,
+                                   int64_t *vs, double *cs, double *es, cudaStream_t s);
+
+cudaError_t launch_dft2_f64(int count, int M, int N, const double *in, double *out, int inverse,
+                            double *tmp, cudaStream_t s);
+cudaError_t launch_build_weight_f64(int count, int M, int N, const int8_t *labels, double rho,
+                                    double *w, cudaStream_t s);
+cudaError_t launch_select_basis_f64(int M, int N, const double *R, int64_t *uv, cudaStream_t s);
+cudaError_t launch_update_residual_f64(int M, int N, double *R, const double *W, int u, int v,
+                                       double cr, double ci, cudaStream_t s);
+
+// ------------------------------------------------------------ class setup
+// Per geometry class: w (fp64) from labels, W = DFT(w) in fp64, exact
+// Hermitian symmetrisation, and the fast kernel's table layouts.
+struct ClassSetupArgs {
+  int n_classes, F;
+  double rho;
+  const int8_t *labels;   // n_classes x F x F
+  double *W64;            // n_classes x F x F c128 (symmetrised spectrum)
+  double *w64;            // n_classes x F x F (weights)
+  float *wtab;            // n_classes x F x F (weights, fp32)
+  void *fast_table;       // n_classes x fast_table_bytes(F) (may be null)
+  size_t fast_table_bytes;
+  double *w00;            // n_classes
+  double *tmp;            // n_classes x F x F c128 scratch
+};
+cudaError_t launch_class_setup(const ClassSetupArgs &a, cudaStream_t s);
+
+// ------------------------------------------------------------------ fast
+// Fused register-resident fp32 kernel for F in {32, 64, 128}.
+struct FastArgs {
+  int F, B, border, iterations;
+  float gamma;
+  int n_rounds;
+  const int32_t *rounds;       // n_rounds x slots block ids (-1 = idle)
+  const int32_t *round_class;  // n_rounds
+  const int32_t *blocks;       // n_blocks x 3 (frame, top, left)
+  const float *wtab;           // n_classes x F x F
+  const void *table;           // n_classes x table_bytes
+  size_t table_bytes;
+  const float *inv_w00;        // n_classes
+  const int32_t *support_rect; // n_classes x 4 (r0, c0, r1, c1) window coords
+  const void *frames;
+  int dtype;
+  long long pitch, frame_stride;
+  int H, W;
+  void *tiles;
+  int tile_dtype;
+  int32_t *trace_uv;
+  float *trace_c, *trace_e;
+};
+struct FastConfig {
+  int slots, threads, smem_bytes, grid;
+  size_t table_bytes;
+};
+// Returns false when F is not supported by the fused kernel.
+bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg);
+cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, cudaStream_t s);
+
+// ------------------------------------------------------------- image f64
+// Gather F x F windows (f64, zero outside the image) for a list of blocks.
+cudaError_t launch_gather_windows(const void *frames, int dtype, long long pitch,
+                                  long long frame_stride, int H, int W, const int32_t *blocks,
+                                  int n, int F, int B, double *windows, cudaStream_t s);
+// Copy the B x B loss tiles out of reconstructed windows into tiles.
+cudaError_t launch_extract_tiles(const double *recon, int n, int F, int B, void *tiles,
+                                 int tile_dtype, cudaStream_t s);
+
+}  // namespace fse

@@ -1,0 +1,263 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Run on a B200: pytest -m gpu."""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests import _golden
+from tests._windows import fp32_gate, window_of
+
+pytestmark = pytest.mark.gpu
+
+CASES = _golden.all_cases()
+
+
+@pytest.fixture(scope="module")
+def fse(cuda_ok):
+    import paper_2204_14193_b200 as fse
+    return fse
+
+
+# ------------------------------------------------------------ fp64 path
+
+
+@pytest.mark.parametrize("c", CASES, ids=[c["name"] for c in CASES])
+def test_extrapolate_fp64_matches_reference(fse, c):
+    """fp64 gate (north_star): selection sequence identical (modulo the exact
+    conjugate-mirror symmetry), pixels within 1e-9."""
+    M, N = c["signal"].shape
+    cfg = fse.FseConfig(rho_hat=c["rho"], gamma=c["gamma"], iterations=max(c["iterations"], 1),
+                        fft_dims=(M, N), basis_target=c["iterations"] if c["iterations"] == 0 else None)
+    mask = fse.AreaMask(c["labels"])
+    r = fse.extrapolate_cfse(c["signal"], mask, cfg)
+    loss = c["labels"] == 2
+    np.testing.assert_allclose(r.reconstructed[loss], c["recon_loss"], rtol=0, atol=1e-9)
+    assert np.array_equal(r.reconstructed[~loss], c["signal"][~loss])  # bit-identical
+    assert r.basis_count == c["iterations"] == len(r.trace)
+    us = np.array([t.frequency[0] for t in r.trace], np.int64)
+    vs = np.array([t.frequency[1] for t in r.trace], np.int64)
+    cs = np.array([t.coefficient for t in r.trace], np.complex128)
+    es = np.array([t.residual_energy for t in r.trace])
+    kind, info = orc.trace_equivalence(_golden.trace(c), (us, vs, cs), M, N)
+    assert kind != "diverged", (kind, info)
+    if c["iterations"]:
+        np.testing.assert_allclose(es, c["es"], rtol=1e-9, atol=1e-9 * c["e0"])
+    if "model" in c:
+        np.testing.assert_allclose(r.model, c["model"], rtol=0, atol=1e-9)
+
+
+def test_fp64_canonical_fraction(fse):
+    """Report how many golden windows match the reference raw vs mirrored."""
+    kinds = {}
+    for c in CASES:
+        if c["iterations"] == 0:
+            continue
+        M, N = c["signal"].shape
+        cfg = fse.FseConfig(rho_hat=c["rho"], gamma=c["gamma"], iterations=c["iterations"], fft_dims=(M, N))
+        out = fse.extrapolate_cfse_batch(c["signal"][None], c["labels"], cfg)
+        tr = (out["us"][0].cpu().numpy(), out["vs"][0].cpu().numpy(), out["cs"][0].cpu().numpy())
+        k, _ = orc.trace_equivalence(_golden.trace(c), tr, M, N)
+        kinds[k] = kinds.get(k, 0) + 1
+    print("fp64 trace agreement vs reference:", kinds)
+    assert "diverged" not in kinds
+
+
+def test_cfse_kernel_bitwise_on_reference_spectra(fse):
+    """Given the reference's own spectra, the GPU loop reproduces the numba
+    loop bit for bit (unfused IEEE order)."""
+    n = 0
+    for c in CASES:
+        if "R_w" not in c:
+            continue
+        R = c["R_w"].copy()
+        G, us, vs, cs, es = fse.cfse_kernel(R, c["W"], c["gamma"], 1.0 / c["w00"], c["iterations"], c["e0"])
+        assert np.array_equal(us, c["us"]) and np.array_equal(vs, c["vs"]), c["name"]
+        assert np.array_equal(cs, c["cs"]), c["name"]
+        assert np.array_equal(es, c["es"]), c["name"]
+        R2 = c["R_w"].copy()
+        G2, *_ = orc.cfse_kernel(R2, c["W"], c["gamma"], 1.0 / c["w00"], c["iterations"], c["e0"])
+        assert np.array_equal(R, R2), "final residual differs from the numba-order oracle"
+        assert np.array_equal(G, G2)
+        n += 1
+    assert n >= 5
+
+
+def test_spectral_ops(fse):
+    rng = np.random.default_rng(1)
+    for shape in [(8, 8), (12, 10), (64, 64), (1, 7)]:
+        x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        X = fse.dft2(x)
+        np.testing.assert_allclose(X, np.fft.fft2(x), rtol=0, atol=1e-10 * np.abs(X).max())
+        np.testing.assert_allclose(fse.idft2(X), x, rtol=0, atol=1e-10 * np.abs(x).max())
+    lab = orc.build_mask((64, 64), (24, 24, 16, 16), 16)
+    w = fse.build_weight(fse.AreaMask(lab), 0.8)
+    np.testing.assert_allclose(w, orc.build_weight(lab, 0.8), rtol=1e-14, atol=0)
+    W = fse.weight_spectrum(w)
+    assert abs(W[0, 0].real - 48.97836003129341) < 1e-12 * 48.98
+
+
+def test_step_ops(fse):
+    rng = np.random.default_rng(2)
+    R = rng.standard_normal((16, 12)) + 1j * rng.standard_normal((16, 12))
+    k = int(np.argmax(np.abs(R) ** 2))
+    assert fse.select_basis(R) == divmod(k, 12)
+    R[3, 3] = R[5, 1] = 100.0  # tie -> first in row-major order
+    assert fse.select_basis(R) == (3, 3)
+    assert fse.select_basis(np.zeros((4, 4), complex)) == (0, 0)
+    W = rng.standard_normal((16, 12)) + 1j * rng.standard_normal((16, 12))
+    R1, R2 = R.copy(), R.copy()
+    fse.update_residual(R1, W, 5, 7, 0.3 - 0.2j)
+    R2 -= (0.3 - 0.2j) * np.roll(W, (5, 7), axis=(0, 1))
+    np.testing.assert_allclose(R1, R2, rtol=0, atol=1e-12)
+    G = np.zeros((8, 8), complex)
+    fse.update_model(G, 1, 2, 1 + 1j)
+    assert G[1, 2] == 64 + 64j
+    assert fse.estimate_coefficient(np.full((2, 2), 10.0), 0, 0, 0.2, 1 / 5.0) == pytest.approx(0.4)
+
+
+def test_errors(fse):
+    cfg = fse.FseConfig(fft_dims=(64, 64))
+    mask = fse.build_mask((64, 64), (24, 24, 16, 16), 16)
+    with pytest.raises(fse.ConfigError):
+        fse.extrapolate_cfse(np.zeros((32, 32)), mask, cfg)
+    s = np.zeros((64, 64)); s[0, 0] = np.nan
+    with pytest.raises(ValueError):
+        fse.extrapolate_cfse(s, mask, cfg)
+    with pytest.raises(ValueError):
+        fse.extrapolate_cfse([[1j] * 64] * 64, mask, cfg)
+    with pytest.raises(fse.ConfigError):  # loss block outside the image
+        fse.ConcealPlan(np.array([[0, 250, 0]]), 256, 256)
+
+
+# ------------------------------------------------------- fused fp32 path
+
+
+def _run_plan(fse, frames, blocks, F, B, border, iters, prec="fp32", tile="f32", trace=True):
+    import torch
+    plan = fse.ConcealPlan(blocks, frames.shape[-2], frames.shape[-1], fse.Geometry(B, border, F),
+                           rho_hat=0.8, gamma=0.5, iterations=iters, precision=prec)
+    fr = torch.from_numpy(np.ascontiguousarray(frames)).cuda()
+    out = plan.run(fr, tile_dtype=tile, trace=trace and prec == "fp32")
+    if trace and prec == "fp32":
+        tiles, tr = out
+        uv = tr["uv"].cpu().numpy(); c = tr["c"].cpu().numpy()
+        get = lambda k: (uv[k, :, 0].astype(np.int64), uv[k, :, 1].astype(np.int64),
+                         c[k, :, 0] + 1j * c[k, :, 1])
+        return tiles.cpu().numpy(), get, plan
+    return out.cpu().numpy(), None, plan
+
+
+def _truth(frames, blocks, B):
+    fr = frames if frames.ndim == 3 else frames[None]
+    return np.stack([fr[f, t:t + B, l:l + B] for f, t, l in blocks]).astype(np.float64)
+
+
+def test_config2_fp32(fse):
+    """Config 2: 512x512 f32 1/f^2 field, 256 blocks at (32i, 32j)."""
+    from paper_2204_14193_b200.synth import field, grid_blocks
+    img = field(512, 512, seed=2).astype(np.float32)
+    tl = grid_blocks(512, 512, 16)
+    blocks = np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
+    tiles, get, plan = _run_plan(fse, img, blocks, 64, 16, 16, 100)
+    assert plan.info["fast_path"] == 1 and plan.info["n_classes"] == 4
+    st = fp32_gate(img, blocks, tiles, get, 64, 16, 16, 0.8, 0.5, 100, truth=_truth(img, blocks, 16))
+    print("config2", st)
+
+
+def test_config4a_fp32(fse):
+    from paper_2204_14193_b200.synth import field
+    img = field(512, 512, seed=4).astype(np.float32)
+    tl = np.array([(16 * i, 16 * j) for i in range(32) for j in range(32)], np.int32)[::2][:500]
+    tl = tl[np.lexsort((tl[:, 1], tl[:, 0]))]
+    blocks = np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
+    tiles, get, plan = _run_plan(fse, img, blocks, 32, 8, 8, 100)
+    assert plan.info["fast_path"] == 1
+    st = fp32_gate(img, blocks, tiles, get, 32, 8, 8, 0.8, 0.5, 100, truth=_truth(img, blocks, 8))
+    print("config4a", st)
+
+
+def test_config4b_fp32(fse):
+    from paper_2204_14193_b200.synth import field
+    imgs = np.stack([field(512, 512, seed=40 + k) for k in range(2)]).astype(np.float32)
+    blocks = np.array([(f, 64 * i, 64 * j) for f in range(2) for i in range(8) for j in range(8)],
+                      np.int32)[:100]
+    tiles, get, plan = _run_plan(fse, imgs, blocks, 128, 32, 16, 100)
+    assert plan.info["fast_path"] == 1
+    st = fp32_gate(imgs, blocks, tiles, get, 128, 32, 16, 0.8, 0.5, 100, truth=_truth(imgs, blocks, 32))
+    print("config4b", st)
+
+
+def test_config3_u8_subset_fp32(fse):
+    """Config 3 geometry (1920x1080 u8 + edges, 10% isolated loss, I=200) on 2 frames."""
+    from paper_2204_14193_b200.synth import frame_u8
+    frames = np.stack([frame_u8(1080, 1920, seed=300 + f) for f in range(2)])
+    blocks = fse.frames_pattern(2, 1080, 1920, 16, 0.10, seed=3)
+    assert len(blocks) == 2 * 804
+    sub = blocks[::4]
+    tiles, get, plan = _run_plan(fse, frames, sub, 64, 16, 16, 200)
+    st = fp32_gate(frames, sub, tiles, get, 64, 16, 16, 0.8, 0.5, 200, truth=_truth(frames, sub, 16))
+    print("config3", st)
+
+
+def test_fp64_plan_matches_oracle(fse):
+    """fp64 image-level path (config 1 + clipped blocks): tiles within 1e-9."""
+    from paper_2204_14193_b200.synth import field
+    img = field(256, 256, seed=1)
+    blocks = np.array([[0, 120, 120], [0, 0, 0], [0, 240, 16], [0, 96, 240]], np.int32)
+    tiles, _, plan = _run_plan(fse, img, blocks, 64, 16, 16, 100, prec="fp64", tile="f64")
+    assert plan.info["fast_path"] == 0
+    ref = orc.conceal_blocks(img, blocks, 16, 16, 64, 0.8, 0.5, 100)
+    np.testing.assert_allclose(tiles, ref, rtol=0, atol=1e-9)
+    # and config 1 against the reference's own golden output
+    c = _golden.load("config1.npz")[0]
+    np.testing.assert_allclose(tiles[0].ravel(), c["recon_loss"], rtol=0, atol=1e-9)
+
+
+def test_u8_tiles_and_edge_cases(fse):
+    import torch
+    from paper_2204_14193_b200.synth import frame_u8
+    fr = frame_u8(256, 384, seed=9)
+    blocks = np.array([[0, 0, 0], [0, 0, 368], [0, 240, 0], [0, 240, 368], [0, 128, 192]], np.int32)
+    t32, _, _ = _run_plan(fse, fr, blocks, 64, 16, 16, 100, tile="f32", trace=False)
+    t8, _, _ = _run_plan(fse, fr, blocks, 64, 16, 16, 100, tile="u8", trace=False)
+    assert t8.dtype == np.uint8
+    assert np.array_equal(t8, np.rint(np.clip(t32, 0, 255)).astype(np.uint8))
+    # padded pitch: same frame inside a wider allocation
+    big = torch.zeros((1, 256, 512), dtype=torch.uint8, device="cuda")
+    big[0, :, :384] = torch.from_numpy(fr).cuda()
+    plan = fse.ConcealPlan(blocks, 256, 384, fse.Geometry(16, 16, 64), gamma=0.5, iterations=100)
+    tp = plan.run(big[:, :, :384], tile_dtype="f32").cpu().numpy()
+    assert np.array_equal(tp, t32)
+    # determinism
+    t32b, _, _ = _run_plan(fse, fr, blocks, 64, 16, 16, 100, tile="f32", trace=False)
+    assert np.array_equal(t32, t32b)
+    # empty block list and iterations = 0 (basis_target 0: loss -> 0)
+    e, _, _ = _run_plan(fse, fr, np.zeros((0, 3), np.int32), 64, 16, 16, 100, trace=False)
+    assert e.shape == (0, 16, 16)
+    z, _, _ = _run_plan(fse, fr, blocks, 64, 16, 16, 0, trace=False)
+    assert np.all(z == 0)
+
+
+def test_concealer_host_pipeline(fse):
+    from paper_2204_14193_b200.synth import frame_u8
+    frames = np.stack([frame_u8(270, 480, seed=50 + f) for f in range(5)])
+    blocks = fse.frames_pattern(5, 270, 480, 16, 0.05, seed=7)
+    con = fse.Concealer(blocks, 5, 270, 480, chunk_frames=2, iterations=100, gamma=0.5,
+                        tile_dtype="f32")
+    out = con.run(con.pin(frames))
+    ref_plan, _, _ = _run_plan(fse, frames, blocks, 64, 16, 16, 100, trace=False)
+    assert np.array_equal(out, ref_plan)
+
+
+def test_conceal_image_api(fse):
+    from paper_2204_14193_b200.synth import frame_u8
+    img = frame_u8(128, 128, seed=3)
+    pat = fse.loss_pattern(128, 128, 16, 6, seed=1)
+    cfg = fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=100, fft_dims=(64, 64), precision="fp32")
+    out, tiles = fse.conceal(img, pat, cfg)
+    mask = np.zeros(img.shape, bool)
+    for t, l in pat:
+        mask[t:t + 16, l:l + 16] = True
+    assert np.array_equal(out[~mask], img[~mask])  # only loss samples change
+    p = fse.psnr(img, out, pat, 16)
+    assert 10 < p < 60
