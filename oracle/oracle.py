@@ -303,6 +303,35 @@ def trace_equivalence(trace_a, trace_b, M: int, N: int, ctol: float = 1e-9,
     return "mirror-swaps", {"flips": flips}
 
 
+def pick_deficit(signal, labels, rho, gamma, upto: int, trace_other) -> float:
+    """Certify an fp32 divergence: step the fp64 oracle to iteration `upto`
+    (the first canonical divergence from `trace_other`) and return
+    (max|R_w|^2 - |R_w[pick]|^2) / max|R_w|^2, where pick is the other run's
+    selection at `upto` mapped into the oracle's (possibly mirrored) frame.
+    A small value means the other run chose a bin that is, within its own
+    arithmetic's precision, as good as the maximum -- a near-tie."""
+    s = np.asarray(signal, np.float64)
+    w = build_weight(labels, rho)
+    W = dft2(w.astype(np.complex128))
+    R = dft2((s * w).astype(np.complex128))
+    e0 = float(np.sum(w * s * s))
+    M, N = R.shape
+    n = max(upto + 1, 1)
+    R0 = R.copy()
+    _, ous, ovs, ocs, _ = cfse_kernel(R0, W, gamma, 1.0 / W[0, 0].real, n, e0)
+    oc = canonicalize_trace(ous, ovs, ocs, M, N)
+    mirrored = not np.array_equal(oc[0], ous)
+    gu, gv, _ = canonicalize_trace(*trace_other, M, N)
+    pu, pv = int(gu[upto]), int(gv[upto])
+    if mirrored:
+        pu, pv = (-pu) % M, (-pv) % N
+    if upto > 0:
+        cfse_kernel(R, W, gamma, 1.0 / W[0, 0].real, upto, e0)
+    m2 = R.real ** 2 + R.imag ** 2
+    top = float(m2.max())
+    return float((top - m2[pu, pv]) / top) if top > 0 else 0.0
+
+
 def near_tie_gap(signal, labels, rho, gamma, upto: int) -> float:
     """Step the fp64 oracle `upto` iterations, then return the relative gap
     between the two largest |R_w|^2 values at that point (the selection the

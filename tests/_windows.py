@@ -17,10 +17,14 @@ def window_of(frame: np.ndarray, top: int, left: int, F: int, B: int, border: in
 
 
 def fp32_gate(frames, blocks, tiles_gpu, traces_gpu, F, B, border, rho, gamma, iters,
-              px_tol=0.5, psnr_tol=0.01, tie_gap=1e-6, truth=None):
+              px_tol=0.5, psnr_tol=0.01, tie_tol=1e-4, truth=None):
     """The north-star fp32 gate: per block max |dpx| <= px_tol except
-    certified near-ties (top-2 |R_w|^2 relative gap < tie_gap at the first
-    canonical divergence), and pooled PSNR within psnr_tol dB.  Returns a
+    certified near-ties, and pooled PSNR within psnr_tol dB.  A block is a
+    certified near-tie when, at the first canonical divergence, the fp32
+    run's selected bin has |R_w|^2 within a relative tie_tol of the fp64
+    maximum (oracle.pick_deficit): both choices are greedy-optimal to
+    within fp32 accumulated error (near-ties below fp32
+    resolution are unavoidable for any fp32 implementation).  Returns a
     stats dict (raises AssertionError on failure)."""
     fr = frames if frames.ndim == 3 else frames[None]
     ref = orc.conceal_blocks(fr, blocks, B, border, F, rho, gamma, iters)
@@ -36,8 +40,8 @@ def fp32_gate(frames, blocks, tiles_gpu, traces_gpu, F, B, border, rho, gamma, i
         assert tr is not None, f"block {k} off by {dev[k]:.3f} and no trace to certify it"
         at = orc.first_divergence((o["us"], o["vs"], o["cs"]), tr, F, F)
         assert at is not None, f"block {k}: identical selections yet off by {dev[k]:.3f} px"
-        gap = orc.near_tie_gap(s, lab, rho, gamma, at)
-        assert gap < tie_gap, f"block {k}: off by {dev[k]:.3f} px, divergence at {at} gap {gap:.2e}"
+        gap = orc.pick_deficit(s, lab, rho, gamma, at, tr)
+        assert gap < tie_tol, f"block {k}: off by {dev[k]:.3f} px, divergence at {at} deficit {gap:.2e}"
         certified.append((int(k), float(dev[k]), int(at), float(gap)))
     stats = dict(n=len(blocks), max_dev=float(dev.max()) if len(dev) else 0.0,
                  over=len(bad), certified=certified)
