@@ -13,7 +13,7 @@ import re
 from .errors import ConfigError, FseError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libfse_b200.so")
+SO_PATH = os.environ.get("FSE_LIB_PATH") or os.path.join(HERE, "libfse_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "fse_b200.h")
 
 FSE_OK = 0

@@ -34,18 +34,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(os.path.join(HERE, d)) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> str:
+    """Compile the library.  `defines`/`out` build diagnostic variants
+    (e.g. FSE_DIAG) next to the product library; the product is SO."""
+    target = os.path.abspath(out) if out else SO
+    if not force and out is None and up_to_date():
         return SO
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    cmd = [nvcc(), *ARCH, *[f"-D{d}" for d in defines], "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-I", os.path.join(REPO, "include"),
-           "-o", SO + ".tmp", *[os.path.join(HERE, s) for s in SOURCES]]
+           "-o", target + ".tmp", *[os.path.join(HERE, s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=HERE)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

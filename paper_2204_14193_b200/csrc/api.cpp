@@ -84,9 +84,11 @@ struct fse_plan {
   double rho = 0, gamma = 0;
   int n_classes = 0, n_rounds = 0;
   bool fast = false;
+  int stagger_ns = 0;
   fse::FastConfig cfg{};
   // device
   int32_t *blocks = nullptr, *rounds = nullptr, *round_class = nullptr, *block_class = nullptr;
+  int32_t *rects = nullptr;  // n_classes x (r0, c0, r1, c1): clipped support rectangle
   int8_t *labels = nullptr;
   float *wtab = nullptr, *inv_w00 = nullptr;
   void *table = nullptr;
@@ -281,6 +283,8 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
   CK(p->alloc(&p->blocks, (size_t)n_blocks * 3));
   CK(p->alloc(&p->block_class, (size_t)n_blocks));
   CK(p->alloc(&p->labels, labels.size()));
+  CK(p->alloc(&p->rects, (size_t)std::max(nc, 1) * 4));
+  if (nc) CK(cudaMemcpyAsync(p->rects, rects.data(), (size_t)nc * 4 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   CK(p->alloc(&p->wtab, (size_t)nc * FF));
   CK(p->alloc(&p->inv_w00, (size_t)nc));
   CK(p->alloc(&p->W64, (size_t)nc * FF * 2));
@@ -296,6 +300,7 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
   p->fast = precision == FSE_PREC_F32 && fse::fast_config(F, iterations, sm_count(), &p->cfg) &&
             B * B == 2 * (F * F / 32) && iterations > 0;
   if (p->fast) CK(p->alloc((char **)&p->table, (size_t)nc * p->cfg.table_bytes));
+  if (const char *e = getenv("FSE_STAGGER_NS")) p->stagger_ns = atoi(e);
 
   fse::ClassSetupArgs ca{};
   ca.n_classes = nc; ca.F = F; ca.rho = rho; ca.labels = p->labels; ca.W64 = p->W64;
@@ -392,10 +397,11 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.F = p->F; a.B = p->B; a.border = p->border; a.iterations = p->iterations;
     a.gamma = (float)p->gamma; a.n_rounds = p->n_rounds; a.rounds = p->rounds;
     a.round_class = p->round_class; a.blocks = p->blocks; a.wtab = p->wtab; a.table = p->table;
-    a.table_bytes = p->cfg.table_bytes; a.inv_w00 = p->inv_w00; a.support_rect = nullptr;
+    a.table_bytes = p->cfg.table_bytes; a.inv_w00 = p->inv_w00; a.support_rect = p->rects;
     a.frames = frames; a.dtype = dtype; a.pitch = pitch; a.frame_stride = frame_stride;
     a.H = p->H; a.W = p->W; a.tiles = tiles; a.tile_dtype = tile_dtype;
     a.trace_uv = trace_uv; a.trace_c = (float *)trace_c; a.trace_e = (float *)trace_e;
+    a.stagger_ns = p->stagger_ns;
     CK(fse::launch_fast(a, p->cfg, st));
     return FSE_OK;
   }

@@ -45,11 +45,29 @@ template <int F> struct FG {
   static constexpr int TROWS = F == 32 ? F + 31 : F == 64 ? F + 15 : F + 7;
   static constexpr size_t TABLE_BYTES =
       PLANAR ? (size_t)TROWS * F * 2 * sizeof(float) : (size_t)TROWS * F * sizeof(float4);
-  static constexpr size_t SCRATCH = (size_t)F * F * sizeof(float2);
+  // FFT scratch: radix-2 in place (F = 128) or the real half-spectrum scheme
+  // (F <= 64: max(F/2 x (F+1), F x (F/2+1)) complex, padded rows)
+  static constexpr size_t SCRATCH =
+      F == 128 ? (size_t)F * F * sizeof(float2)
+               : (((size_t)F * (F / 2 + 1) * sizeof(float2) + 15) & ~(size_t)15);
+  static constexpr int TRACE_CAP = F == 128 ? 1 << 30 : (int)(SCRATCH / 16);
   static constexpr size_t REGION = ALIAS ? (TABLE_BYTES > SCRATCH ? TABLE_BYTES : SCRATCH) : TABLE_BYTES;
 };
 
 FSE_DEV float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// acc = a * b + acc with the accumulator as a read-write PTX operand.  With
+// the intrinsic form ptxas writes the result into the (dead) W' register
+// pair and pays ~30 MOVs per iteration to rotate the loop-carried spectrum
+// back into place; the tied operand keeps it in place.
+FSE_DEV void ffma2_acc(float2 &acc, float2 a, float b) {
+  unsigned long long r, x;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(acc.x), "f"(acc.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+  unsigned long long bb;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(b));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(x), "l"(bb));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(r));
+}
 FSE_DEV float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
 template <int F> struct SlotPtrs {
@@ -96,19 +114,20 @@ template <int F> FSE_DEV void decode_bin(int idx, int w, int &p, int &mem, int &
   }
 }
 
-#define FSE_PICK(P)                 \
-  case P:                           \
-    rr = Rre[P];                    \
-    ri = Rim[P];                    \
+#define FSE_PICK(P)                           \
+  case P:                                     \
+    re = mem ? Rre[P].y : Rre[P].x;           \
+    im = mem ? Rim[P].y : Rim[P].x;           \
     break;
 
-// warp-uniform p: one indirect branch instead of a 16-way select chain
-FSE_DEV void pick_pair(const float2 (&Rre)[16], const float2 (&Rim)[16], int p, float2 &rr,
-                       float2 &ri) {
+// Value of bin (pair p, member mem) of this thread; p is warp-uniform, so
+// the switch is a uniform branch, not a 16-way select chain.
+FSE_DEV void pick_bin(const float2 (&Rre)[16], const float2 (&Rim)[16], int p, int mem, float &re,
+                      float &im) {
   switch (p) {
     FSE_PICK(0) FSE_PICK(1) FSE_PICK(2) FSE_PICK(3) FSE_PICK(4) FSE_PICK(5) FSE_PICK(6)
     FSE_PICK(7) FSE_PICK(8) FSE_PICK(9) FSE_PICK(10) FSE_PICK(11) FSE_PICK(12) FSE_PICK(13)
-    FSE_PICK(14) default: rr = Rre[15]; ri = Rim[15]; break;
+    FSE_PICK(14) default: re = mem ? Rre[15].y : Rre[15].x; im = mem ? Rim[15].y : Rim[15].x; break;
   }
 }
 
@@ -153,6 +172,76 @@ FSE_DEV void slot_fft(float2 *S, const float2 *tw, int st, int slot) {
   }
 }
 
+
+// ------------------------------------------------ radix-8 register FFT
+FSE_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+FSE_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+FSE_DEV float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+FSE_DEV float2 cmi(float2 a) { return make_float2(a.y, -a.x); }  // -i * a
+
+// In-register forward DFT-8 (natural order in and out).
+FSE_DEV void dft8(float2 (&x)[8]) {
+  const float s = 0.70710678118654752f;
+  float2 a0 = cadd(x[0], x[4]), a4 = csub(x[0], x[4]);
+  float2 a1 = cadd(x[1], x[5]), a5 = csub(x[1], x[5]);
+  float2 a2 = cadd(x[2], x[6]), a6 = csub(x[2], x[6]);
+  float2 a3 = cadd(x[3], x[7]), a7 = csub(x[3], x[7]);
+  a5 = make_float2(s * (a5.x + a5.y), s * (a5.y - a5.x));    // * e^{-i pi/4}
+  a6 = cmi(a6);                                               // * -i
+  a7 = make_float2(s * (a7.y - a7.x), -s * (a7.x + a7.y));    // * e^{-3i pi/4}
+  float2 b0 = cadd(a0, a2), b2 = csub(a0, a2), b1 = cadd(a1, a3), b3 = cmi(csub(a1, a3));
+  float2 b4 = cadd(a4, a6), b6 = csub(a4, a6), b5 = cadd(a5, a7), b7 = cmi(csub(a5, a7));
+  x[0] = cadd(b0, b1); x[4] = csub(b0, b1); x[2] = cadd(b2, b3); x[6] = csub(b2, b3);
+  x[1] = cadd(b4, b5); x[5] = csub(b4, b5); x[3] = cadd(b6, b7); x[7] = csub(b6, b7);
+}
+
+FSE_DEV void dft4(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+  float2 a0 = cadd(x0, x2), a2 = csub(x0, x2), a1 = cadd(x1, x3), a3 = cmi(csub(x1, x3));
+  x0 = cadd(a0, a1); x1 = cadd(a2, a3); x2 = csub(a0, a1); x3 = csub(a2, a3);
+}
+
+// Length-F forward FFT by a group of Q = F/8 lanes of one warp.  Lane t
+// holds x[t + Q k] (k < 8) in v; on return it holds X[q1 + 8 q2] for its
+// q1 set (Q = 8: q1 = t; Q = 4: q1 in {t, t+4}) in v[q2] (Q = 8) or
+// v[q2] (q1 = t) / v[4 + q2] (q1 = t + 4) for Q = 4.  `ex` is this group's
+// exchange area (8*Q complex, element (q1, t) at ex[q1 * Q + t]).
+template <int F>
+FSE_DEV void group_fft(float2 (&v)[8], float2 *ex, int es, const float2 *tw, int t) {
+  constexpr int Q = F / 8;
+  dft8(v);
+#pragma unroll
+  for (int q1 = 1; q1 < 8; ++q1) v[q1] = cmul(v[q1], tw[t * q1]);
+#pragma unroll
+  for (int q1 = 0; q1 < 8; ++q1) ex[(q1 * Q + t) * es] = v[q1];
+  __syncwarp();
+  if (Q == 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = ex[(t * Q + k) * es];
+    dft8(v);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = ex[(t * Q + k) * es];
+      v[4 + k] = ex[((t + 4) * Q + k) * es];
+    }
+    dft4(v[0], v[1], v[2], v[3]);
+    dft4(v[4], v[5], v[6], v[7]);
+  }
+  __syncwarp();
+}
+
+// the two warp synchronisations of group_fft, for lanes with no FFT to do
+FSE_DEV void group_fft_idle() {
+  __syncwarp();
+  __syncwarp();
+}
+
+// output index of v[i] after group_fft for lane t
+template <int F> FSE_DEV int group_out(int t, int i) {
+  if (F == 64) return t + 8 * i;
+  return (i < 4) ? t + 8 * i : (t + 4) + 8 * (i - 4);
+}
+
 // Cooperative copy of one class's table (global -> shared), 16 B per op.
 FSE_DEV void copy_table(void *dst, const void *src, size_t bytes, int tid, int nthr) {
   const uint4 *s = (const uint4 *)src;
@@ -166,8 +255,8 @@ __global__ void __launch_bounds__(512, 1) fast_kernel(FastArgs a, int iter_cap) 
   extern __shared__ __align__(16) char smem[];
   char *region = smem;
   float2 *syn_tw = (float2 *)(smem + G::REGION);  // exp(+2 pi i j / F), j < F
-  float2 *fft_tw = syn_tw + F;                     // exp(-2 pi i j / F), j < F/2
-  char *slots_base = (char *)(fft_tw + F / 2);
+  float2 *fft_tw = syn_tw + F;                     // exp(-2 pi i j / F), j < F
+  char *slots_base = (char *)(fft_tw + F);
   const size_t slot_bytes =
       (G::ALIAS ? 0 : G::SCRATCH) + 2 * G::NW * sizeof(uint4) + 64 +
       (G::ALIAS ? (size_t)iter_cap * sizeof(float4) : 0);
@@ -186,12 +275,13 @@ __global__ void __launch_bounds__(512, 1) fast_kernel(FastArgs a, int iter_cap) 
     double s, c;
     sincospi(2.0 * j / F, &s, &c);
     syn_tw[j] = make_float2((float)c, (float)s);
-    if (j < F / 2) fft_tw[j] = make_float2((float)c, (float)-s);
+    fft_tw[j] = make_float2((float)c, (float)-s);
   }
   __syncthreads();
 
   const int off = (F - a.B) / 2;
   int loaded = -1;
+  bool first = true;
   for (int round = blockIdx.x; round < a.n_rounds; round += gridDim.x) {
     const int cls = __ldg(a.round_class + round);
     if (!G::ALIAS && cls != loaded) {
@@ -200,6 +290,14 @@ __global__ void __launch_bounds__(512, 1) fast_kernel(FastArgs a, int iter_cap) 
                  blockDim.x);
       __syncthreads();
       loaded = cls;
+    }
+    if (first) {
+      // The slots of a CTA do identical work; started together (the table
+      // load above is a CTA barrier) they stay in lock-step, so their
+      // setup and reduction phases coincide.  Offsetting their start lets
+      // one slot's latency-bound phases overlap another's throughput work.
+      first = false;
+      if (a.stagger_ns > 0 && slot > 0) __nanosleep((unsigned)(slot * a.stagger_ns));
     }
     const int b = __ldg(a.rounds + (size_t)round * G::S + slot);
     if (G::S == 1 && b < 0) continue;  // uniform for a single slot
@@ -212,37 +310,139 @@ __global__ void __launch_bounds__(512, 1) fast_kernel(FastArgs a, int iter_cap) 
     const float *wtab = a.wtab + (size_t)cls * F * F;
     const size_t fbase = (size_t)fidx * (size_t)a.frame_stride;
     float e0p = 0.f;
-    for (int i = st; i < F * F; i += G::NT) {
-      const int m = i >> G::LOG, n = i & (F - 1);
-      const int y = wt + m, x = wl + n;
-      const float wv = __ldg(wtab + i);
-      float v = 0.f;
-      if (wv != 0.f && y >= 0 && y < a.H && x >= 0 && x < a.W) {
-        const float s = load_px(a.frames, a.dtype, fbase + (size_t)y * a.pitch + x);
-        v = s * wv;
-        e0p += v * s;
-      }
-      const int rm = __brev(m) >> (32 - G::LOG), rn = __brev(n) >> (32 - G::LOG);
-      sp.scratch[rm * F + rn] = make_float2(v, 0.f);
-    }
-    slot_sync<F>(slot);
-    slot_fft<F>(sp.scratch, fft_tw, st, slot);
-
-    // ------------------------------- R_w -> registers, exactly Hermitian
     float2 Rre[16], Rim[16];
-#pragma unroll
-    for (int p = 0; p < 16; ++p) {
-      float2 xa, xb, ma, mb;
-      {
-        const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
-        const int ra = ia >> G::LOG, ca = ia & (F - 1), rb = ib >> G::LOG, cb = ib & (F - 1);
-        xa = sp.scratch[ia];
-        xb = sp.scratch[ib];
-        ma = sp.scratch[((F - ra) & (F - 1)) * F + ((F - ca) & (F - 1))];
-        mb = sp.scratch[((F - rb) & (F - 1)) * F + ((F - cb) & (F - 1))];
+    if constexpr (F == 128) {
+      for (int i = st; i < F * F; i += G::NT) {
+        const int m = i >> G::LOG, n = i & (F - 1);
+        const int y = wt + m, x = wl + n;
+        const float wv = __ldg(wtab + i);
+        float v = 0.f;
+        if (wv != 0.f && y >= 0 && y < a.H && x >= 0 && x < a.W) {
+          const float s = load_px(a.frames, a.dtype, fbase + (size_t)y * a.pitch + x);
+          v = s * wv;
+          e0p += v * s;
+        }
+        const int rm = __brev(m) >> (32 - G::LOG), rn = __brev(n) >> (32 - G::LOG);
+        sp.scratch[rm * F + rn] = make_float2(v, 0.f);
       }
-      Rre[p] = make_float2((xa.x + ma.x) * 0.5f, (xb.x + mb.x) * 0.5f);
-      Rim[p] = make_float2((xa.y - ma.y) * 0.5f, (xb.y - mb.y) * 0.5f);
+      slot_sync<F>(slot);
+      slot_fft<F>(sp.scratch, fft_tw, st, slot);
+      // R_w -> registers, exactly Hermitian
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        float2 xa, xb, ma, mb;
+        {
+          const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
+          const int ra = ia >> G::LOG, ca = ia & (F - 1), rb = ib >> G::LOG, cb = ib & (F - 1);
+          xa = sp.scratch[ia];
+          xb = sp.scratch[ib];
+          ma = sp.scratch[((F - ra) & (F - 1)) * F + ((F - ca) & (F - 1))];
+          mb = sp.scratch[((F - rb) & (F - 1)) * F + ((F - cb) & (F - 1))];
+        }
+        Rre[p] = make_float2((xa.x + ma.x) * 0.5f, (xb.x + mb.x) * 0.5f);
+        Rim[p] = make_float2((xa.y - ma.y) * 0.5f, (xb.y - mb.y) * 0.5f);
+      }
+    } else {
+      // Real-input 2-D FFT, half spectrum (F in {32, 64}):
+      //   rows   -- row pairs packed as one complex row, z_j = x_2j + i x_2j+1,
+      //             one length-F FFT per pair (only pairs meeting the support);
+      //   columns -- columns 1..F/2-1 of the untangled row spectra, plus
+      //             columns 0 and F/2 packed as one complex column;
+      //   the other half follows from X[k][l] = conj(X[-k][-l]), so R_w is
+      //   exactly Hermitian by construction.
+      // Each length-F FFT is radix 8 x Q in registers of Q = F/8 lanes with
+      // one shared-memory exchange (group_fft).
+      constexpr int Q = F / 8, NG = G::NT / Q, H = F / 2, ZS = F + 1, XS = H + 1, CP = H / NG;
+      const int g = st / Q, t = st - (st / Q) * Q;
+      float2 *S = sp.scratch;
+      const int4 rect = __ldg((const int4 *)a.support_rect + cls);  // (r0, c0, r1, c1)
+      const int j0 = rect.x >> 1, j1 = (rect.z + 1) >> 1;
+      // warp-uniform trip count: every lane of a warp takes part in each
+      // group_fft (it synchronises the warp); idle groups transform zeros
+      for (int jb = j0; jb < j1; jb += NG) {
+        const int j = jb + g;
+        const bool act = j < j1;
+        float2 v[8];
+        const int y0 = wt + 2 * j;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int n = t + Q * k, x = wl + n;
+          float xe = 0.f, xo = 0.f;
+          if (act && x >= 0 && x < a.W) {
+            const float we = __ldg(wtab + (2 * j) * F + n), wo = __ldg(wtab + (2 * j + 1) * F + n);
+            if (we != 0.f && y0 >= 0 && y0 < a.H) {
+              const float s = load_px(a.frames, a.dtype, fbase + (size_t)y0 * a.pitch + x);
+              xe = s * we;
+              e0p += xe * s;
+            }
+            if (wo != 0.f && y0 + 1 >= 0 && y0 + 1 < a.H) {
+              const float s = load_px(a.frames, a.dtype, fbase + (size_t)(y0 + 1) * a.pitch + x);
+              xo = s * wo;
+              e0p += xo * s;
+            }
+          }
+          v[k] = make_float2(xe, xo);
+        }
+        float2 *row = S + j * ZS;
+        if (act) {
+          group_fft<F>(v, row, 1, fft_tw, t);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) row[group_out<F>(t, i)] = v[i];
+        } else {
+          group_fft_idle();
+        }
+      }
+      slot_sync<F>(slot);
+      float2 cin[CP][8];
+#pragma unroll
+      for (int pass = 0; pass < CP; ++pass) {
+        const int c = g + pass * NG;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int m = t + Q * k, j = m >> 1, odd = m & 1;
+          float2 y = make_float2(0.f, 0.f);
+          if (j >= j0 && j < j1) {
+            if (c == 0) {
+              const float2 z0 = S[j * ZS], zh = S[j * ZS + H];
+              y = odd ? make_float2(z0.y, zh.y) : make_float2(z0.x, zh.x);
+            } else {
+              const float2 zl = S[j * ZS + c], zm = S[j * ZS + F - c];
+              y = odd ? make_float2((zl.y + zm.y) * 0.5f, (zm.x - zl.x) * 0.5f)
+                      : make_float2((zl.x + zm.x) * 0.5f, (zl.y - zm.y) * 0.5f);
+            }
+          }
+          cin[pass][k] = y;
+        }
+      }
+      slot_sync<F>(slot);  // the row spectra are consumed; reuse as X
+#pragma unroll
+      for (int pass = 0; pass < CP; ++pass) {
+        const int c = g + pass * NG;
+        group_fft<F>(cin[pass], S + c, XS, fft_tw, t);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) S[group_out<F>(t, i) * XS + c] = cin[pass][i];
+      }
+      slot_sync<F>(slot);
+      auto bin = [&](int r, int c) -> float2 {
+        if (c == 0 || c == H) {  // untangle the packed real columns 0 and F/2
+          const float2 yk = S[r * XS], ym = S[((F - r) & (F - 1)) * XS];
+          return c == 0 ? make_float2((yk.x + ym.x) * 0.5f, (yk.y - ym.y) * 0.5f)
+                        : make_float2((yk.y + ym.y) * 0.5f, (ym.x - yk.x) * 0.5f);
+        }
+        if (c < H) return S[r * XS + c];
+        const float2 z = S[((F - r) & (F - 1)) * XS + (F - c)];
+        return make_float2(z.x, -z.y);
+      };
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
+        const float2 xa = bin(ia >> G::LOG, ia & (F - 1)), xb = bin(ib >> G::LOG, ib & (F - 1));
+        // an arithmetic op gives each SoA pair a fresh, aligned register
+        // pair (plain copies let the allocator split the pairs and pay MOVs
+        // around every FFMA2 of the hot loop)
+        Rre[p] = __fadd2_rn(make_float2(xa.x, xb.x), make_float2(0.f, 0.f));
+        Rim[p] = __fadd2_rn(make_float2(xa.y, xb.y), make_float2(0.f, 0.f));
+      }
     }
     // e0 = sum w s^2 (slot reduction; trace energies only)
     for (int o = 16; o; o >>= 1) e0p += __shfl_xor_sync(0xffffffffu, e0p, o);
@@ -276,14 +476,18 @@ __global__ void __launch_bounds__(512, 1) fast_kernel(FastArgs a, int iter_cap) 
         for (int p = 0; p < 16; ++p) {
           const float4 wv = tp[(F == 32 ? 2 * p : p) * F];
           const float2 wr = make_float2(wv.x, wv.y), wi = make_float2(wv.z, wv.w);
-          Rre[p] = ffma2(wr, make_float2(-cre, -cre), Rre[p]);
-          Rre[p] = ffma2(wi, make_float2(cim, cim), Rre[p]);
-          Rim[p] = ffma2(wi, make_float2(-cre, -cre), Rim[p]);
-          Rim[p] = ffma2(wr, make_float2(-cim, -cim), Rim[p]);
+          ffma2_acc(Rre[p], wr, -cre);
+          ffma2_acc(Rre[p], wi, cim);
+          ffma2_acc(Rim[p], wi, -cre);
+          ffma2_acc(Rim[p], wr, -cim);
           float2 mg = fmul2(Rre[p], Rre[p]);
           mg = ffma2(Rim[p], Rim[p], mg);
           const float m = fmaxf(mg.x, mg.y);
+#if FSE_DIAG & 2
+          best = fmaxf(best, m);
+#else
           if (m > best) { best = m; bp = p; bx = mg.x; }
+#endif
         }
       } else {
         const float *Tre = (const float *)region;
@@ -297,10 +501,10 @@ __global__ void __launch_bounds__(512, 1) fast_kernel(FastArgs a, int iter_cap) 
           const int q = 2 * (p & 1);
           const float2 wr = make_float2(Tre[r + co[q]], Tre[r + co[q + 1]]);
           const float2 wi = make_float2(Tim[r + co[q]], Tim[r + co[q + 1]]);
-          Rre[p] = ffma2(wr, make_float2(-cre, -cre), Rre[p]);
-          Rre[p] = ffma2(wi, make_float2(cim, cim), Rre[p]);
-          Rim[p] = ffma2(wi, make_float2(-cre, -cre), Rim[p]);
-          Rim[p] = ffma2(wr, make_float2(-cim, -cim), Rim[p]);
+          ffma2_acc(Rre[p], wr, -cre);
+          ffma2_acc(Rre[p], wi, cim);
+          ffma2_acc(Rim[p], wi, -cre);
+          ffma2_acc(Rim[p], wr, -cim);
           float2 mg = fmul2(Rre[p], Rre[p]);
           mg = ffma2(Rim[p], Rim[p], mg);
           const float m = fmaxf(mg.x, mg.y);
@@ -314,12 +518,16 @@ __global__ void __launch_bounds__(512, 1) fast_kernel(FastArgs a, int iter_cap) 
       const unsigned widx = __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
       int pw, mw, ow;
       decode_bin<F>((int)widx, w, pw, mw, ow);
-      float2 rr, ri;
-      pick_pair(Rre, Rim, pw, rr, ri);
-      float are = __shfl_sync(0xffffffffu, mw ? rr.y : rr.x, ow);
-      float aim = __shfl_sync(0xffffffffu, mw ? ri.y : ri.x, ow);
+      float are, aim;
+      pick_bin(Rre, Rim, pw, mw, are, aim);
+      are = __shfl_sync(0xffffffffu, are, ow);
+      aim = __shfl_sync(0xffffffffu, aim, ow);
       unsigned gidx = widx, gkey = wmax;
+#if FSE_DIAG & 1
+      if (false) {
+#else
       if (G::NW > 1) {
+#endif
         uint4 *xc = sp.xch + parity * G::NW;
         if (lane == 0) xc[w] = make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim));
         slot_sync<F>(slot);
@@ -393,8 +601,7 @@ template <int F> static size_t fast_smem(int iter_cap) {
   typedef FG<F> G;
   size_t slot_bytes = (G::ALIAS ? 0 : G::SCRATCH) + 2 * G::NW * sizeof(uint4) + 64 +
                       (G::ALIAS ? (size_t)iter_cap * sizeof(float4) : 0);
-  return G::REGION + (size_t)F * sizeof(float2) + (size_t)(F / 2) * sizeof(float2) +
-         G::S * slot_bytes;
+  return G::REGION + 2 * (size_t)F * sizeof(float2) + G::S * slot_bytes;
 }
 
 bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
@@ -402,11 +609,11 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
   int S;
   switch (F) {
     case 32:
-      if (iterations > 32 * 32 / 2) return false;
+      if (iterations > FG<32>::TRACE_CAP) return false;
       smem = fast_smem<32>(0); tb = FG<32>::TABLE_BYTES; S = FG<32>::S;
       break;
     case 64:
-      if (iterations > 64 * 64 / 2) return false;
+      if (iterations > FG<64>::TRACE_CAP) return false;
       smem = fast_smem<64>(0); tb = FG<64>::TABLE_BYTES; S = FG<64>::S;
       break;
     case 128:

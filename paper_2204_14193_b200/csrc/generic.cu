@@ -28,7 +28,6 @@
 namespace fse {
 
 constexpr int kGenThreads = 512;
-constexpr int kGenWarps = kGenThreads / 32;
 
 __device__ double block_max_abs(const double *x, int n, double *red) {
   double v = 0.0;

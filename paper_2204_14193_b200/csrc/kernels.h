@@ -77,6 +77,7 @@ struct FastArgs {
   int tile_dtype;
   int32_t *trace_uv;
   float *trace_c, *trace_e;
+  int stagger_ns;  // start offset per slot (desynchronises the slots' reduction phases)
 };
 struct FastConfig {
   int slots, threads, smem_bytes, grid;

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+for d in 0 1 2 3; do
+  if [ $d = 0 ]; then L=""; else L="$PWD/paper_2204_14193_b200/_diag/diag$d.so"; fi
+  FSE_LIB_PATH=$L timeout 300 python bench.py --steps 5 --warmup 2 --no-e2e --no-cpu --frames 64 > gpurun_out/diag_$d.log 2>&1
+  echo "diag=$d $(python -c "import json,sys; d=json.loads(open('gpurun_out/diag_$d.log').read().strip().splitlines()[-1]); print(round(d['value']/1e6,3), 'Mblk/s', round(d['roofline']['frac'],3))")"
+done
