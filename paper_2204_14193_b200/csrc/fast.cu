@@ -37,8 +37,11 @@ template <int F> struct FG {
   static constexpr int NW = NT / 32;      // warps per slot
   static constexpr int CPL = F / 32;      // columns per lane
   static constexpr int RPW = 32 / CPL;    // rows per warp
-  static constexpr int S = F == 32 ? 16 : F == 64 ? 4 : 1;
-  static constexpr int CTA = NT * S;      // 512
+#ifndef FSE_SLOTS64
+#define FSE_SLOTS64 5
+#endif
+  static constexpr int S = F == 32 ? 16 : F == 64 ? FSE_SLOTS64 : 1;
+  static constexpr int CTA = NT * S;      // threads per CTA
   static constexpr bool PLANAR = F == 128;  // planar re/im table (pair table would not fit)
   static constexpr bool ALIAS = F == 128;   // FFT scratch and table share one region
   // rows of the row-extended table: the thread walks rows rowoff + step*p
@@ -250,7 +253,7 @@ FSE_DEV void copy_table(void *dst, const void *src, size_t bytes, int tid, int n
 }
 
 template <int F>
-__global__ void __launch_bounds__(512, 1) fast_kernel(FastArgs a, int iter_cap) {
+__global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int iter_cap) {
   typedef FG<F> G;
   extern __shared__ __align__(16) char smem[];
   char *region = smem;
@@ -624,7 +627,7 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
   }
   if (smem > 227 * 1024) return false;
   cfg->slots = S;
-  cfg->threads = 512;
+  cfg->threads = F == 32 ? FG<32>::CTA : F == 64 ? FG<64>::CTA : FG<128>::CTA;
   cfg->smem_bytes = (int)smem;
   cfg->grid = sm_count;
   cfg->table_bytes = tb;

@@ -20,11 +20,10 @@ for fn in funcs[1:]:
     fi = [i for i, l in enumerate(ins) if "FFMA2" in l]
     first, last = fi[0], fi[-1]
     end = tgt = None
-    for i in range(last, len(ins)):
-        m = re.search(r"BRA (0x[0-9a-f]+)", ins[i])
-        if m and int(m.group(1), 16) <= addr(ins[first]):
+    for i in range(last, len(ins)):  # innermost backward branch around the FFMA2 block
+        m = re.search(r"BRA(?:\.U)?\s+(?:!?U?P\w+,\s*)?(0x[0-9a-f]+)", ins[i])
+        if m and int(m.group(1), 16) <= addr(ins[first]) and (tgt is None or int(m.group(1), 16) > tgt):
             tgt, end = int(m.group(1), 16), i
-            break
     start = [i for i, l in enumerate(ins) if addr(l) == tgt][0]
     body = ins[start:end + 1]
     c = collections.Counter(re.sub(r"^\s*/\*[0-9a-f]+\*/\s*(@!?U?P\w+\s+)?", "", l).split()[0].split(".")[0]
