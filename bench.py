@@ -56,12 +56,6 @@ def dist_env():
     return rank, world, local
 
 
-def shard(n_frames: int, rank: int, world: int):
-    f0 = n_frames * rank // world
-    f1 = n_frames * (rank + 1) // world
-    return f0, f1
-
-
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -218,12 +212,11 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    f0, f1 = shard(cfg["frames"], rank, world)
-    nf = f1 - f0
+    from paper_2204_14193_b200 import sharding
+
     all_blocks = make_blocks(cfg, cfg["frames"])
-    sel = (all_blocks[:, 0] >= f0) & (all_blocks[:, 0] < f1)
-    blocks = all_blocks[sel].copy()
-    blocks[:, 0] -= f0
+    sh = sharding.shard_blocks(all_blocks, cfg["frames"], rank, world)
+    f0, nf, blocks = sh.f0, sh.n_frames, sh.blocks
     frames = field_torch(nf, cfg["H"], cfg["W"], seed=SEED * 7919 + f0, device="cuda")
     geo = fse.Geometry(cfg["B"], cfg["border"], cfg["F"])
     plan = fse.ConcealPlan(blocks, cfg["H"], cfg["W"], geo, rho_hat=RHO, gamma=GAMMA,
