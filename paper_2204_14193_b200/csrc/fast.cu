@@ -91,6 +91,9 @@ template <int F> FSE_DEV void slot_sync(int slot) {
 }
 
 FSE_DEV float load_px(const void *frames, int dtype, size_t idx) {
+#if FSE_DIAG & 4
+  return 100.f + (float)(idx & 7);
+#endif
   if (dtype == 0) return (float)__ldg((const uint8_t *)frames + idx);
   if (dtype == 1) return __ldg((const float *)frames + idx);
   return (float)__ldg((const double *)frames + idx);
@@ -362,6 +365,9 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
       const int j0 = rect.x >> 1, j1 = (rect.z + 1) >> 1;
       // warp-uniform trip count: every lane of a warp takes part in each
       // group_fft (it synchronises the warp); idle groups transform zeros
+#if FSE_DIAG & 16
+      if (false)
+#endif
       for (int jb = j0; jb < j1; jb += NG) {
         const int j = jb + g;
         const bool act = j < j1;
@@ -418,6 +424,9 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         }
       }
       slot_sync<F>(slot);  // the row spectra are consumed; reuse as X
+#if FSE_DIAG & 16
+      if (false)
+#endif
 #pragma unroll
       for (int pass = 0; pass < CP; ++pass) {
         const int c = g + pass * NG;
@@ -589,6 +598,9 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
       pn[k] = off + q % a.B;
       g[k] = 0.f;
     }
+#if FSE_DIAG & 8
+    if (false)
+#endif
 #pragma unroll 2
     for (int it = 0; it < a.iterations; ++it) {
       const float4 tr = sp.trace[it];
@@ -596,9 +608,19 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
       const int tu = (int)(uv & 0xffffu), tv = (int)(uv >> 16);
 #pragma unroll
       for (int k = 0; k < PX; ++k) {
+#ifdef FSE_SYN_SFU
+        // exact integer phase, centred to [-F/2, F/2) so the SFU argument
+        // stays in [-pi, pi) where __sincosf is most accurate (~1e-6 abs)
+        const int j = ((tu * pm[k] + tv * pn[k] + F / 2) & (F - 1)) - F / 2;
+        float sn, cs;
+        __sincosf((float)j * (6.283185307179586f / F), &sn, &cs);
+        g[k] = fmaf(tr.y, cs, g[k]);
+        g[k] = fmaf(-tr.z, sn, g[k]);
+#else
         const float2 t = syn_tw[(tu * pm[k] + tv * pn[k]) & (F - 1)];
         g[k] = fmaf(tr.y, t.x, g[k]);
         g[k] = fmaf(-tr.z, t.y, g[k]);
+#endif
       }
     }
 #pragma unroll
