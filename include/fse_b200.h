@@ -49,6 +49,7 @@ extern "C" {
 /* per-window status written by fse_extrapolate (device int32) */
 #define FSE_STATUS_OK 0
 #define FSE_STATUS_EMPTY_SUPPORT 1 /* w00 <= 1e-12*M*N, cfse.py:47-48 */
+#define FSE_STATUS_DEGENERATE_PAIRS 2 /* rFSE pair Gram singular, rfse.py:50-54 */
 
 /* Library version string and last error message (thread-local). */
 const char *fse_version(void);
@@ -100,6 +101,21 @@ int fse_extrapolate(int count, int M, int N, int precision, const double *signal
                     const int8_t *labels, long long labels_stride, double rho, double gamma,
                     int iterations, double *recon, double *model, int64_t *us, int64_t *vs,
                     double *cs, double *es, int32_t *status, void *stream);
+
+/* Drop-in for `extrapolate_rfse(signal, mask, config)` (rfse.py:170-210),  */
+/* the paper's real-valued conjugate-pair variant: per iteration the joint  */
+/* projection of every bin onto {phi, conj(phi)} (per-bin 2x2 Gram solve,   */
+/* self-conjugate bins as one real atom), canonical pair member, two-term   */
+/* residual update.  max_iters / stop_tally follow rfse.py:182-187          */
+/* (fixed count: max_iters = I, stop_tally = 2I+1; basis_target T: both T). */
+/* Trace arrays hold max_iters entries; counts/tallies (int32[count]) give  */
+/* the executed iterations and the basis-function tally; selfs marks        */
+/* self-conjugate selections.  Same layout/ownership as fse_extrapolate.    */
+int fse_extrapolate_rfse(int count, int M, int N, int precision, const double *signal,
+                         const int8_t *labels, long long labels_stride, double rho, double gamma,
+                         int max_iters, int stop_tally, double *recon, double *model, int64_t *us,
+                         int64_t *vs, double *cs, double *es, int32_t *selfs, int32_t *counts,
+                         int32_t *tallies, int32_t *status, void *stream);
 
 /* Single-step ops of cfse.py:145-178 on device (SPEC test surface).       */
 /* select_basis: argmax |R|^2, first max in row-major order -> uv[0..1].   */

@@ -13,8 +13,10 @@ from .weighting import Area, AreaMask, build_mask, build_weight, weight_spectrum
 from .spectral import basis_function, dft2, idft2
 from .cfse import (cfse_kernel, estimate_coefficient, extrapolate_cfse, extrapolate_cfse_batch,
                    select_basis, update_model, update_residual)
-from .harness import (Concealer, ConcealPlan, Geometry, conceal, conceal_frames, loss_pattern,
-                      loss_pattern_fraction, frames_pattern, psnr, psnr_tiles, write_tiles)
+from .harness import (Concealer, ConcealPlan, Geometry, conceal, conceal_frames, grid_pattern,
+                      loss_pattern, loss_pattern_fraction, frames_pattern, psnr, psnr_tiles,
+                      write_tiles)
+from .rfse import RfsePlan, conceal_frames_rfse, extrapolate_rfse, extrapolate_rfse_batch
 
 __all__ = [
     "ConfigError", "FseError", "PgmError", "ALGORITHMS", "ExtrapolationResult", "FseConfig",
@@ -22,5 +24,6 @@ __all__ = [
     "basis_function", "dft2", "idft2", "cfse_kernel", "estimate_coefficient", "extrapolate_cfse",
     "extrapolate_cfse_batch", "select_basis", "update_model", "update_residual", "Concealer",
     "ConcealPlan", "Geometry", "conceal", "conceal_frames", "loss_pattern", "loss_pattern_fraction",
-    "frames_pattern", "psnr", "psnr_tiles", "write_tiles",
+    "frames_pattern", "psnr", "psnr_tiles", "write_tiles", "grid_pattern", "RfsePlan",
+    "conceal_frames_rfse", "extrapolate_rfse", "extrapolate_rfse_batch",
 ]

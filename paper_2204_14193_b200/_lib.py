@@ -53,6 +53,7 @@ _SIGS = {
     "fse_build_weight_f64": ([I, I, I, P, D, P, P], I),
     "fse_cfse_kernel_f64": ([I, I, I, P, P, LL, D, P, I, P, P, P, P, P, P, P], I),
     "fse_extrapolate": ([I, I, I, I, P, P, LL, D, D, I, P, P, P, P, P, P, P, P], I),
+    "fse_extrapolate_rfse": ([I, I, I, I, P, P, LL, D, D, I, I, P, P, P, P, P, P, P, P, P, P, P], I),
     "fse_select_basis_f64": ([I, I, P, P, P], I),
     "fse_update_residual_f64": ([I, I, P, P, I, I, D, D, P], I),
     "fse_plan_create": ([ctypes.POINTER(P), P, I, I, I, I, I, I, D, D, I, I, P], I),

@@ -198,6 +198,49 @@ int fse_extrapolate(int count, int M, int N, int precision, const double *signal
   return FSE_OK;
 }
 
+int fse_extrapolate_rfse(int count, int M, int N, int precision, const double *signal,
+                         const int8_t *labels, long long labels_stride, double rho, double gamma,
+                         int max_iters, int stop_tally, double *recon, double *model, int64_t *us,
+                         int64_t *vs, double *cs, double *es, int32_t *selfs, int32_t *counts,
+                         int32_t *tallies, int32_t *status, void *stream) {
+  if (int r = check_dims(M, N)) return r;
+  if (int r = check_rho_gamma(rho, gamma)) return r;
+  if (max_iters < 0 || stop_tally < 0) return fail(FSE_ERR_CONFIG, "iterations must be >= 0");
+  if (precision != FSE_PREC_F64 && precision != FSE_PREC_F32)
+    return fail(FSE_ERR_UNSUPPORTED, "precision %d", precision);
+  if (count <= 0) return FSE_OK;
+  if (!signal || !labels || !recon || !status || !counts || !tallies ||
+      (max_iters > 0 && (!us || !vs || !cs || !es || !selfs)))
+    return fail(FSE_ERR_VALUE, "null pointer");
+  const int chunk = 2048;
+  for (int c0 = 0; c0 < count; c0 += chunk) {
+    int n = std::min(chunk, count - c0);
+    fse::GenArgs a{};
+    a.count = n; a.M = M; a.N = N; a.iterations = max_iters; a.precision = precision;
+    a.rho = rho; a.gamma = gamma; a.algorithm = 1; a.stop_tally = stop_tally;
+    a.signal = signal + (size_t)c0 * M * N;
+    a.labels = labels + (size_t)c0 * labels_stride;
+    a.labels_stride = labels_stride;
+    a.recon = recon + (size_t)c0 * M * N;
+    a.model = model ? model + (size_t)c0 * 2 * M * N : nullptr;
+    a.us = us ? us + (size_t)c0 * max_iters : nullptr;
+    a.vs = vs ? vs + (size_t)c0 * max_iters : nullptr;
+    a.cs = cs ? cs + (size_t)c0 * 2 * max_iters : nullptr;
+    a.es = es ? es + (size_t)c0 * max_iters : nullptr;
+    a.selfs = selfs ? selfs + (size_t)c0 * max_iters : nullptr;
+    a.counts = counts + c0;
+    a.tallies = tallies + c0;
+    a.status = status + c0;
+    size_t ws = fse::generic_workspace_bytes(n, M, N, precision);
+    void *wsp = nullptr;
+    if (ws) CK(cudaMallocAsync(&wsp, ws, S(stream)));
+    cudaError_t e = fse::launch_generic_extrapolate(a, wsp, S(stream));
+    if (wsp) cudaFreeAsync(wsp, S(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "extrapolate_rfse");
+  }
+  return FSE_OK;
+}
+
 int fse_select_basis_f64(int M, int N, const double *R, int64_t *uv, void *stream) {
   if (int r = check_dims(M, N)) return r;
   CK(fse::launch_select_basis_f64(M, N, R, uv, S(stream)));

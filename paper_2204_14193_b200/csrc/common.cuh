@@ -19,11 +19,13 @@ template <> struct Ieee<double> {
   static FSE_DEV double mul(double a, double b) { return __dmul_rn(a, b); }
   static FSE_DEV double add(double a, double b) { return __dadd_rn(a, b); }
   static FSE_DEV double sub(double a, double b) { return __dsub_rn(a, b); }
+  static FSE_DEV double div(double a, double b) { return __ddiv_rn(a, b); }
 };
 template <> struct Ieee<float> {
   static FSE_DEV float mul(float a, float b) { return __fmul_rn(a, b); }
   static FSE_DEV float add(float a, float b) { return __fadd_rn(a, b); }
   static FSE_DEV float sub(float a, float b) { return __fsub_rn(a, b); }
+  static FSE_DEV float div(float a, float b) { return __fdiv_rn(a, b); }
 };
 
 template <typename T> struct Cplx { T re, im; };

@@ -185,6 +185,120 @@ __device__ void cfse_iterate(Cplx<T> *R, const Cplx<T> *W, int M, int N, T gamma
   __syncthreads();
 }
 
+// rFSE loop (rfse.py:58-167): per iteration a scan of every bin with the
+// joint projection onto the conjugate pair {phi, conj(phi)} (variable
+// denominators D = w00^2 - |W[2k,2l]|^2, self-conjugate bins on their own
+// branch), selection of the maximal exact energy decrease, canonical pair
+// member, and a two-term residual update.  Unfused IEEE ops in the numba
+// order, so fp64 results are bit-identical given the same spectra.
+template <typename T>
+__device__ void rfse_iterate(Cplx<T> *R, const Cplx<T> *W, int M, int N, T gamma, T w00,
+                             int max_iters, int stop_tally, double e0, int64_t *us, int64_t *vs,
+                             double *cs, double *es, int32_t *selfs, int32_t *out_count,
+                             int32_t *out_tally, T *sv, int *si, double4 *bcast) {
+  typedef Ieee<T> F;
+  const int MN = M * N;
+  const T damp = F::mul(gamma, F::sub((T)2.0, gamma));
+  const T w00sq = F::mul(w00, w00);
+  T e = (T)e0;
+  int count = 0, tally = 0;
+  while (count < max_iters && tally < stop_tally) {
+    T best = (T)-1.0;
+    int bi = 0;
+    for (int i = threadIdx.x; i < MN; i += blockDim.x) {
+      const int k = i / N, l = i - k * N;
+      const Cplx<T> a = R[i];
+      T crit;
+      if ((2 * k) % M == 0 && (2 * l) % N == 0) {
+        const T pr = F::div(a.re, w00);
+        crit = F::mul(a.re, pr);
+      } else {
+        const Cplx<T> w2 = W[((2 * k) % M) * N + (2 * l) % N];
+        const T nr = F::sub(F::mul(w00, a.re), F::add(F::mul(w2.re, a.re), F::mul(w2.im, a.im)));
+        const T ni = F::sub(F::mul(w00, a.im), F::sub(F::mul(w2.im, a.re), F::mul(w2.re, a.im)));
+        const T d = F::sub(w00sq, F::add(F::mul(w2.re, w2.re), F::mul(w2.im, w2.im)));
+        const T pr = F::div(nr, d), pi = F::div(ni, d);
+        crit = F::mul((T)2.0, F::add(F::mul(pr, a.re), F::mul(pi, a.im)));
+      }
+      if (crit > best) { best = crit; bi = i; }
+    }
+    block_argmax(best, bi, sv, si);
+    if (threadIdx.x == 0) bcast[0] = make_double4((double)best, 0.0, 0.0, __longlong_as_double((long long)bi));
+    __syncthreads();
+    const double4 b0 = bcast[0];
+    const int idx = (int)__double_as_longlong(b0.w);
+    const T bestv = (T)b0.x;
+    int u = idx / N, v = idx - u * N;
+    const bool bself = (2 * u) % M == 0 && (2 * v) % N == 0;
+    // the projection of the winner, recomputed by every thread (identical ops)
+    T bpr, bpi;
+    {
+      const Cplx<T> a = R[idx];
+      if (bself) {
+        bpr = F::div(a.re, w00);
+        bpi = (T)0.0;
+      } else {
+        const Cplx<T> w2 = W[((2 * u) % M) * N + (2 * v) % N];
+        const T nr = F::sub(F::mul(w00, a.re), F::add(F::mul(w2.re, a.re), F::mul(w2.im, a.im)));
+        const T ni = F::sub(F::mul(w00, a.im), F::sub(F::mul(w2.im, a.re), F::mul(w2.re, a.im)));
+        const T d = F::sub(w00sq, F::add(F::mul(w2.re, w2.re), F::mul(w2.im, w2.im)));
+        bpr = F::div(nr, d);
+        bpi = F::div(ni, d);
+      }
+    }
+    __syncthreads();  // everyone has read R[idx] before it is updated
+    int mu = (M - u) % M, mv = (N - v) % N;
+    if (!bself && mu * N + mv < u * N + v) {  // canonical member (rfse.py:111-121)
+      const int tu = u, tv = v;
+      u = mu; v = mv; mu = tu; mv = tv;
+      bpi = -bpi;
+    }
+    const T cr = F::mul(gamma, bpr), ci = F::mul(gamma, bpi);  // gamma * complex(bpr, bpi)
+    for (int i = threadIdx.x; i < MN; i += blockDim.x) {
+      const int k = i / N, l = i - k * N;
+      int ks = k - u, ls = l - v;
+      if (ks < 0) ks += M;
+      if (ls < 0) ls += N;
+      const Cplx<T> w1 = W[ks * N + ls];
+      Cplx<T> x = R[i];
+      // t1 = c * W[ks, ls]
+      const T t1r = F::sub(F::mul(cr, w1.re), F::mul(ci, w1.im));
+      const T t1i = F::add(F::mul(cr, w1.im), F::mul(ci, w1.re));
+      x.re = F::sub(x.re, t1r);
+      x.im = F::sub(x.im, t1i);
+      if (!bself) {
+        int ks2 = k - mu, ls2 = l - mv;
+        if (ks2 < 0) ks2 += M;
+        if (ls2 < 0) ls2 += N;
+        const Cplx<T> w2 = W[ks2 * N + ls2];
+        // t2 = conj(c) * W[ks2, ls2]
+        const T t2r = F::sub(F::mul(cr, w2.re), F::mul(-ci, w2.im));
+        const T t2i = F::add(F::mul(cr, w2.im), F::mul(-ci, w2.re));
+        x.re = F::sub(x.re, t2r);
+        x.im = F::sub(x.im, t2i);
+      }
+      R[i] = x;
+    }
+    e = F::sub(e, F::mul(damp, bestv));
+    if (threadIdx.x == 0) {
+      us[count] = u;
+      vs[count] = v;
+      cs[2 * count] = (double)cr;
+      cs[2 * count + 1] = (double)ci;
+      es[count] = (double)e;
+      selfs[count] = bself ? 1 : 0;
+    }
+    tally += bself ? 1 : 2;
+    ++count;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out_count = count;
+    *out_tally = tally;
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------- extrapolation
 struct GenLayout {
   bool smem;
@@ -225,7 +339,7 @@ size_t generic_workspace_bytes(int count, int M, int N, int precision) {
   return L.ws_per_window * (size_t)count;
 }
 
-template <typename T>
+template <typename T, int ALG>
 __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, GenLayout L,
                                                                    char *workspace) {
   extern __shared__ __align__(16) char smem[];
@@ -288,6 +402,21 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     if (threadIdx.x == 0) a.status[win] = 1;
     return;
   }
+  if (ALG == 1) {
+    // rfse.py:50-54: pair Gram determinant must not be (nearly) singular
+    int bad = 0;
+    for (int i = threadIdx.x; i < MN; i += blockDim.x) {
+      const int k = i / N, l = i - k * N;
+      if ((2 * k) % M == 0 && (2 * l) % N == 0) continue;
+      const double2 w2 = Bf[((2 * k) % M) * N + (2 * l) % N];
+      const double D = w00 * w00 - (w2.x * w2.x + w2.y * w2.y);
+      if (D <= 1e-9 * w00 * w00) bad = 1;
+    }
+    if (__syncthreads_or(bad)) {
+      if (threadIdx.x == 0) a.status[win] = 2;
+      return;
+    }
+  }
   if (threadIdx.x == 0) a.status[win] = 0;
   const double inv_w00 = 1.0 / w00;
   if (sizeof(T) == sizeof(float)) {
@@ -297,8 +426,16 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     }
     __syncthreads();
   }
-  cfse_iterate<T>(R, Wt, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, nullptr,
-                  (T *)red, redi, bcast);
+  int n_it = a.iterations;
+  if (ALG == 0) {
+    cfse_iterate<T>(R, Wt, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, nullptr,
+                    (T *)red, redi, bcast);
+  } else {
+    rfse_iterate<T>(R, Wt, M, N, (T)a.gamma, (T)w00, a.iterations, a.stop_tally, e0, us, vs, cs, es,
+                    a.selfs + (size_t)win * a.iterations, a.counts + win, a.tallies + win, (T *)red,
+                    redi, bcast);
+    n_it = a.counts[win];
+  }
   // synthesis g = sum c e^{+2 pi i (u m/M + v n/N)} and write-back
   double *rec = a.recon + (size_t)win * MN;
   double *model = a.model ? a.model + (size_t)win * 2 * MN : nullptr;
@@ -307,13 +444,18 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     if (!loss && !model) { rec[i] = s[i]; continue; }
     int m = i / N, n = i - m * N;
     double gr = 0.0, gi = 0.0;
-    for (int it = 0; it < a.iterations; ++it) {
+    for (int it = 0; it < n_it; ++it) {
       int u = (int)us[it], v = (int)vs[it];
       double2 p = twMp[(int)(((long long)u * m) % M)], q = twNp[(int)(((long long)v * n) % N)];
       double pr = p.x * q.x - p.y * q.y, pi = p.x * q.y + p.y * q.x;
       double cr = cs[2 * it], ci = cs[2 * it + 1];
       gr += cr * pr - ci * pi;
       gi += cr * pi + ci * pr;
+      if (ALG == 1 && !a.selfs[(size_t)win * a.iterations + it]) {
+        // the conjugate member: conj(c) * phi_(-u,-v) = conj(c * phi_(u,v))
+        gr += cr * pr - ci * pi;
+        gi -= cr * pi + ci * pr;
+      }
     }
     if (model) { model[2 * i] = gr; model[2 * i + 1] = gi; }
     rec[i] = loss ? gr : s[i];
@@ -324,18 +466,18 @@ cudaError_t launch_generic_extrapolate(const GenArgs &a, void *workspace, cudaSt
   GenLayout L = gen_layout(a.M, a.N, a.precision);
   if (a.count <= 0) return cudaSuccess;
   cudaError_t e;
-  if (a.precision == 1) {
-    e = cudaFuncSetAttribute(extrapolate_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)L.smem_bytes);
-    if (e != cudaSuccess) return e;
-    extrapolate_kernel<float><<<a.count, kGenThreads, L.smem_bytes, st>>>(a, L, (char *)workspace);
-  } else {
-    e = cudaFuncSetAttribute(extrapolate_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)L.smem_bytes);
-    if (e != cudaSuccess) return e;
-    extrapolate_kernel<double><<<a.count, kGenThreads, L.smem_bytes, st>>>(a, L, (char *)workspace);
-  }
-  return cudaGetLastError();
+  auto launch = [&](auto kern) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)L.smem_bytes);
+    if (e2 != cudaSuccess) return e2;
+    kern<<<a.count, kGenThreads, L.smem_bytes, st>>>(a, L, (char *)workspace);
+    return cudaGetLastError();
+  };
+  if (a.algorithm == 1)
+    e = a.precision == 1 ? launch(extrapolate_kernel<float, 1>) : launch(extrapolate_kernel<double, 1>);
+  else
+    e = a.precision == 1 ? launch(extrapolate_kernel<float, 0>) : launch(extrapolate_kernel<double, 0>);
+  return e;
 }
 
 // --------------------------------------------- drop-in for _cfse_kernel

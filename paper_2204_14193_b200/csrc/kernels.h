@@ -19,6 +19,12 @@ struct GenArgs {
   int64_t *us, *vs;
   double *cs, *es;
   int32_t *status;
+  // rFSE only (algorithm = 1): pair-selection trace and stopping rule
+  int algorithm;        // 0 cfse, 1 rfse
+  int stop_tally;       // rfse: stop when the basis-function tally reaches it
+  int32_t *selfs;       // rfse: self-conjugate flag per iteration (count x iterations)
+  int32_t *counts;      // rfse: executed iterations per window
+  int32_t *tallies;     // rfse: basis-function tally per window
 };
 // Size of the global workspace the generic extrapolation needs for `count`
 // windows (0 when everything fits in shared memory).

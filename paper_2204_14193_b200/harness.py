@@ -278,6 +278,20 @@ def psnr_tiles(truth_tiles: np.ndarray, tiles: np.ndarray) -> float:
     return math.inf if mse == 0 else 10.0 * math.log10(255.0 ** 2 / mse)
 
 
+def grid_pattern(H: int, W: int, block: int, stride: int, support: int, seed: int = 0) -> np.ndarray:
+    """SPEC.md:318-324 `generate_pattern`: a deterministic grid of isolated
+    B x B losses every `stride` pixels; the seed only shifts the grid phase
+    (phase = support + seed mod (stride - block - 2 support + 1)).  512x512,
+    stride 64, seed 0 -> 64 blocks at (16 + 64 i, 16 + 64 j)."""
+    if stride < block + 2 * support:
+        raise ConfigError(f"stride {stride} < block + 2*support = {block + 2 * support} (losses not isolated)")
+    span = stride - block - 2 * support + 1
+    ph = support + (int(seed) % span)
+    tops = range(ph, H - block + 1, stride)
+    lefts = range(ph, W - block + 1, stride)
+    return np.array([(t, l) for t in tops for l in lefts], np.int32).reshape(-1, 2)
+
+
 def loss_pattern(H: int, W: int, B: int, count: int, seed: int) -> np.ndarray:
     """Seeded isolated-block loss pattern (native fse_loss_pattern): random
     sequential selection on the B x B grid, no two chosen blocks 8-adjacent.

@@ -17,6 +17,9 @@ def load(name):
         for k in ("rho", "gamma", "w00", "e0"):
             c[k] = float(c[k])
         c["iterations"] = int(c["iterations"])
+        for k in ("tally", "basis_target"):
+            if k in c:
+                c[k] = int(c[k])
         c["name"] = f"{name}:{i}"
         cases.append(c)
     return cases

@@ -24,6 +24,7 @@ sys.path.insert(0, REPO)
 sys.path.insert(0, os.environ.get("FSE_REFERENCE_SRC", "/root/reference/pkg/src"))
 
 from fse.cfse import _prepare, extrapolate_cfse  # noqa: E402  (reference)
+from fse.rfse import extrapolate_rfse  # noqa: E402
 from fse.types import FseConfig  # noqa: E402
 from fse.weighting import AreaMask, build_mask  # noqa: E402
 
@@ -68,6 +69,24 @@ def run(s, mask, rho, gamma, iters, basis_target=None, keep_spectra=False, keep_
     if keep_model:
         rec["model"] = res.model
     return rec
+
+
+def run_rfse(s, mask, rho, gamma, iters, basis_target=None):
+    M, N = s.shape
+    cfg = FseConfig(rho_hat=rho, gamma=gamma, iterations=iters, fft_dims=(M, N), algorithm="rfse",
+                    basis_target=basis_target)
+    res = extrapolate_rfse(s, mask, cfg)
+    _, w, W, w00, R_w, e0 = _prepare(s, mask, cfg)
+    return dict(
+        signal=s, labels=mask.labels, rho=rho, gamma=gamma, iterations=iters,
+        basis_target=-1 if basis_target is None else basis_target,
+        recon_loss=res.reconstructed[mask.loss], tally=res.basis_count, w00=w00, e0=e0,
+        us=np.array([t.frequency[0] for t in res.trace], np.int64),
+        vs=np.array([t.frequency[1] for t in res.trace], np.int64),
+        cs=np.array([t.coefficient for t in res.trace], np.complex128),
+        es=np.array([t.residual_energy for t in res.trace], np.float64),
+        selfs=np.array([t.self_conjugate for t in res.trace], np.int32),
+    )
 
 
 def save(name, cases):
@@ -137,6 +156,25 @@ def main():
     cases.append(run(s, build_mask((64, 64), (24, 24, 16, 16), 16), 0.8, 0.2, 1))
     cases.append(run(s, build_mask((64, 64), (24, 24, 16, 16), 16), 0.8, 0.2, 200))
     save("small.npz", cases)
+
+    # rFSE (rfse.py:170-210), the paper's comparison variant
+    rng = np.random.default_rng(17)
+    cases = []
+    for k in range(6):
+        M = [8, 12, 16][k % 3]
+        s = rng.uniform(0, 255, (M, M))
+        loss = rng.uniform(size=(M, M)) < 0.25
+        cases.append(run_rfse(s, AreaMask.from_loss(loss), 0.8, 0.2, 20))
+    for (t, l) in [(128, 128), (0, 256)]:
+        s, m = window(img4, t, l, 32, 8, 8)
+        cases.append(run_rfse(s, m, rho, gamma, 50))
+    for (t, l) in [(96, 160), (0, 0)]:
+        s, m = window(img2, t, l, 64, 16, 16)
+        cases.append(run_rfse(s, m, rho, gamma, 50))
+    s, m = window(img2, 160, 160, 64, 16, 16)
+    cases.append(run_rfse(s, m, rho, gamma, 50, basis_target=7))
+    cases.append(run_rfse(s, m, rho, gamma, 50, basis_target=0))
+    save("rfse.npz", cases)
 
 
 if __name__ == "__main__":

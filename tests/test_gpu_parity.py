@@ -261,3 +261,47 @@ def test_conceal_image_api(fse):
     assert np.array_equal(out[~mask], img[~mask])  # only loss samples change
     p = fse.psnr(img, out, pat, 16)
     assert 10 < p < 60
+
+
+RFSE = _golden.load("rfse.npz")
+
+
+@pytest.mark.parametrize("c", RFSE, ids=[c["name"] for c in RFSE])
+def test_extrapolate_rfse_fp64_matches_reference(fse, c):
+    """GPU rFSE (rfse.py:170-210) vs the reference's golden outputs: same
+    canonical pair selections, tally, self-conjugate flags; pixels 1e-9."""
+    M, N = c["signal"].shape
+    bt = None if c["basis_target"] < 0 else c["basis_target"]
+    cfg = fse.FseConfig(rho_hat=c["rho"], gamma=c["gamma"], iterations=c["iterations"],
+                        fft_dims=(M, N), algorithm="rfse", basis_target=bt)
+    r = fse.extrapolate_rfse(c["signal"], fse.AreaMask(c["labels"]), cfg)
+    assert r.basis_count == c["tally"]
+    us = np.array([t.frequency[0] for t in r.trace], np.int64)
+    vs = np.array([t.frequency[1] for t in r.trace], np.int64)
+    assert np.array_equal(us, c["us"]) and np.array_equal(vs, c["vs"])
+    assert np.array_equal(np.array([t.self_conjugate for t in r.trace], np.int32), c["selfs"])
+    if len(us):
+        cs = np.array([t.coefficient for t in r.trace])
+        np.testing.assert_allclose(cs, c["cs"], rtol=1e-9, atol=1e-9 * np.abs(c["cs"]).max())
+        np.testing.assert_allclose([t.residual_energy for t in r.trace], c["es"], rtol=1e-9,
+                                   atol=1e-9 * c["e0"])
+    loss = c["labels"] == 2
+    np.testing.assert_allclose(r.reconstructed[loss], c["recon_loss"], rtol=0, atol=1e-9)
+    assert np.array_equal(r.reconstructed[~loss], c["signal"][~loss])
+    assert np.abs(r.model.imag).max() <= 1e-8 * max(np.abs(r.model.real).max(), 1.0)
+
+
+def test_rfse_fp32_and_image_plan(fse):
+    from paper_2204_14193_b200.synth import field
+    img = field(256, 256, seed=8)
+    blocks = np.array([[0, 0, 0], [0, 96, 128], [0, 240, 240]], np.int32)
+    t64 = fse.conceal_frames_rfse(img, blocks, fse.Geometry(16, 16, 64), gamma=0.5, iterations=50)
+    t32 = fse.conceal_frames_rfse(img, blocks, fse.Geometry(16, 16, 64), gamma=0.5, iterations=50,
+                                  precision="fp32")
+    assert np.max(np.abs(t64 - t32)) < 0.5
+    # rFSE and cFSE conceal the same blocks to similar quality (SPEC acceptance 5 proximity)
+    from paper_2204_14193_b200.harness import psnr_tiles
+    tc = fse.conceal_frames(img, blocks, fse.Geometry(16, 16, 64), gamma=0.5, iterations=100,
+                            precision="fp64", tile_dtype="f64")
+    truth = np.stack([img[t:t + 16, l:l + 16] for _, t, l in blocks])
+    assert abs(psnr_tiles(truth, np.clip(t64, 0, 255)) - psnr_tiles(truth, np.clip(tc, 0, 255))) < 1.0

@@ -1,0 +1,73 @@
+"""Harness pieces of SPEC.md:296-427: PGM I/O, grid loss patterns, the `fse`
+CLI (usage/config errors on CPU; a full conceal run on the GPU)."""
+import csv
+import os
+
+import numpy as np
+import pytest
+
+import paper_2204_14193_b200 as fse
+from paper_2204_14193_b200 import cli, pgm
+
+
+def test_pgm_round_trip_and_errors(tmp_path):
+    img = np.array([[0, 128], [255, 7]], np.uint8)
+    p = tmp_path / "a.pgm"
+    pgm.save_image(img, str(p))
+    assert np.array_equal(pgm.load_image(str(p)), img)
+    data = p.read_bytes()
+    assert pgm.dumps(pgm.loads(data)) == data  # byte-identical round trip
+    big = np.random.default_rng(0).integers(0, 256, (512, 512)).astype(np.uint8)
+    assert pgm.dumps(pgm.loads(pgm.dumps(big))) == pgm.dumps(big)
+    assert np.array_equal(pgm.loads(b"P5\n# comment\n2 1\n255\n\x01\x02"), [[1, 2]])
+    with pytest.raises(fse.PgmError, match="byte 0"):
+        pgm.loads(b"P2\n2 2\n255\n0 1 2 3")
+    with pytest.raises(fse.PgmError, match="maxval"):
+        pgm.loads(b"P5\n2 2\n65535\n" + b"\0" * 8)
+    with pytest.raises(fse.PgmError, match="truncated"):
+        pgm.loads(b"P5\n4 4\n255\n" + b"\0" * 3)
+    # saving clamps and rounds half to even
+    assert np.array_equal(pgm.loads(pgm.dumps(np.array([[-3.0, 2.5, 300.0]]))), [[0, 2, 255]])
+
+
+def test_grid_pattern_spec_examples():
+    p = fse.grid_pattern(512, 512, 16, 64, 16, seed=0)
+    assert len(p) == 64 and tuple(p[0]) == (16, 16) and tuple(p[-1]) == (16 + 64 * 7, 16 + 64 * 7)
+    assert len(fse.grid_pattern(64, 64, 16, 64, 16)) == 1
+    assert not np.array_equal(fse.grid_pattern(512, 512, 16, 64, 16, seed=3), p)
+    with pytest.raises(fse.ConfigError):
+        fse.grid_pattern(512, 512, 16, 40, 16)
+
+
+def test_cli_usage_and_config_errors(tmp_path, capsys):
+    with pytest.raises(SystemExit) as e:
+        cli.main(["conceal", "--output", "x.pgm"])  # missing --input
+    assert e.value.code == 2
+    p = tmp_path / "in.pgm"
+    pgm.save_image(np.full((64, 64), 100, np.uint8), str(p))
+    rc = cli.main(["conceal", "--input", str(p), "--output", str(tmp_path / "o.pgm"), "--gamma", "1.5"])
+    assert rc == 2 and "(0, 1]" in capsys.readouterr().err
+    rc = cli.main(["conceal", "--input", str(tmp_path / "missing.pgm"), "--output", "o.pgm"])
+    assert rc == 1
+
+
+@pytest.mark.gpu
+def test_cli_conceal_run(tmp_path, cuda_ok):
+    from paper_2204_14193_b200.synth import frame_u8
+    img = frame_u8(256, 256, seed=4)
+    src, out, rep, dmg = (str(tmp_path / n) for n in ("in.pgm", "out.pgm", "r.csv", "d.pgm"))
+    pgm.save_image(img, src)
+    rc = cli.main(["conceal", "--input", src, "--output", out, "--report", rep, "--damage", dmg,
+                   "--gamma", "0.5", "--iters", "100", "--precision", "fp32"])
+    assert rc == 0
+    res = pgm.load_image(out)
+    pat = fse.grid_pattern(256, 256, 16, 64, 16)
+    mask = np.zeros(img.shape, bool)
+    for t, l in pat:
+        mask[t:t + 16, l:l + 16] = True
+    assert np.array_equal(res[~mask], img[~mask])
+    rows = list(csv.reader(open(rep)))
+    assert rows[0] == ["algo", "bf_count", "block_index", "psnr_db", "sec_per_block"]
+    assert rows[-1][2] == "pooled" and 10 < float(rows[-1][3]) < 60
+    assert (pgm.load_image(dmg)[mask] == 0).all()
+    assert cli.main(["selfcheck"]) == 0

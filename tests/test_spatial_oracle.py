@@ -42,3 +42,21 @@ def test_spatial_oracle_random_instances():
         kinds[k] = kinds.get(k, 0) + 1
         np.testing.assert_allclose(a["reconstructed"], b["reconstructed"], rtol=0, atol=1e-8)
     print(kinds)
+
+
+RFSE_SMALL = [c for c in _golden.load("rfse.npz") if c["signal"].shape[0] <= 16]
+
+
+@pytest.mark.parametrize("c", RFSE_SMALL, ids=[c["name"] for c in RFSE_SMALL])
+def test_spatial_pair_oracle_matches_reference_rfse(c):
+    """pair_mode of the spatial oracle (rfse.py rule, direct sums) against the
+    reference's extrapolate_rfse golden outputs."""
+    o = spatial.extrapolate(c["signal"], c["labels"], c["rho"], c["gamma"], c["iterations"],
+                            pair_mode=True)
+    assert np.array_equal(o["us"], c["us"]) and np.array_equal(o["vs"], c["vs"])
+    np.testing.assert_allclose(o["cs"], c["cs"], rtol=1e-9, atol=1e-9 * np.abs(c["cs"]).max())
+    assert o["tally"] == c["tally"]
+    loss = c["labels"] == 2
+    np.testing.assert_allclose(o["reconstructed"][loss], c["recon_loss"], rtol=0, atol=1e-8)
+    # realness of the pair model (SPEC acceptance 4)
+    assert np.abs(o["model"].imag).max() <= 1e-8 * max(np.abs(o["model"].real).max(), 1.0)
