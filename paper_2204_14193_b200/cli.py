@@ -115,7 +115,7 @@ def _write_csv(path, header, rows):
     w = csv.writer(buf, lineterminator="\n")
     w.writerow(header)
     for r in rows:
-        w.writerow([f"{x:.6f}" if isinstance(x, float) and math.isfinite(x) else x for x in r])
+        w.writerow([f"{x:.6g}" if isinstance(x, float) and math.isfinite(x) else x for x in r])
     if path:
         with open(path, "w") as f:
             f.write(buf.getvalue())

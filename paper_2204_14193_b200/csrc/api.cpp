@@ -92,6 +92,7 @@ struct fse_plan {
   int8_t *labels = nullptr;
   float *wtab = nullptr, *inv_w00 = nullptr;
   void *table = nullptr;
+  float4 *trace_scratch = nullptr;
   double *W64 = nullptr, *w64 = nullptr, *w00 = nullptr, *tmp = nullptr;
   // f64 path workspace
   int chunk = 0;
@@ -343,6 +344,8 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
   p->fast = precision == FSE_PREC_F32 && fse::fast_config(F, iterations, sm_count(), &p->cfg) &&
             B * B == 2 * (F * F / 32) && iterations > 0;
   if (p->fast) CK(p->alloc((char **)&p->table, (size_t)nc * p->cfg.table_bytes));
+  if (p->fast && p->cfg.global_trace)
+    CK(p->alloc(&p->trace_scratch, (size_t)p->cfg.grid * p->cfg.slots * iterations));
   if (const char *e = getenv("FSE_STAGGER_NS")) p->stagger_ns = atoi(e);
 
   fse::ClassSetupArgs ca{};
@@ -445,6 +448,7 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.H = p->H; a.W = p->W; a.tiles = tiles; a.tile_dtype = tile_dtype;
     a.trace_uv = trace_uv; a.trace_c = (float *)trace_c; a.trace_e = (float *)trace_e;
     a.stagger_ns = p->stagger_ns;
+    a.trace_scratch = p->trace_scratch;
     CK(fse::launch_fast(a, p->cfg, st));
     return FSE_OK;
   }

@@ -276,6 +276,8 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
   sp.xch = (uint4 *)(sb + (G::ALIAS ? 0 : G::SCRATCH));
   sp.red = (float *)(sp.xch + 2 * G::NW);
   sp.trace = G::ALIAS ? (float4 *)((char *)sp.red + 64) : (float4 *)sp.scratch;
+  if (a.trace_scratch)  // more iterations than the shared trace holds: per-slot global scratch
+    sp.trace = a.trace_scratch + ((size_t)blockIdx.x * G::S + slot) * a.iterations;
 
   for (int j = tid; j < F; j += blockDim.x) {
     double s, c;
@@ -650,15 +652,17 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
   int S;
   switch (F) {
     case 32:
-      if (iterations > FG<32>::TRACE_CAP) return false;
+      cfg->global_trace = iterations > FG<32>::TRACE_CAP;
       smem = fast_smem<32>(0); tb = FG<32>::TABLE_BYTES; S = FG<32>::S;
       break;
     case 64:
-      if (iterations > FG<64>::TRACE_CAP) return false;
+      cfg->global_trace = iterations > FG<64>::TRACE_CAP;
       smem = fast_smem<64>(0); tb = FG<64>::TABLE_BYTES; S = FG<64>::S;
       break;
     case 128:
-      smem = fast_smem<128>(iterations); tb = FG<128>::TABLE_BYTES; S = FG<128>::S;
+      cfg->global_trace = iterations > 2048;
+      smem = fast_smem<128>(cfg->global_trace ? 0 : iterations); tb = FG<128>::TABLE_BYTES;
+      S = FG<128>::S;
       break;
     default:
       return false;
@@ -679,7 +683,8 @@ template <int F> static cudaError_t launch_fast_t(const FastArgs &a, const FastC
   if (e != cudaSuccess) return e;
   int grid = cfg.grid < a.n_rounds ? cfg.grid : a.n_rounds;
   if (grid <= 0) return cudaSuccess;
-  fast_kernel<F><<<grid, cfg.threads, cfg.smem_bytes, s>>>(a, F == 128 ? a.iterations : 0);
+  fast_kernel<F><<<grid, cfg.threads, cfg.smem_bytes, s>>>(
+      a, (F == 128 && !a.trace_scratch) ? a.iterations : 0);
   return cudaGetLastError();
 }
 

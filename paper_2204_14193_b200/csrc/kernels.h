@@ -84,10 +84,12 @@ struct FastArgs {
   int32_t *trace_uv;
   float *trace_c, *trace_e;
   int stagger_ns;  // start offset per slot (desynchronises the slots' reduction phases)
+  float4 *trace_scratch;  // grid x slots x iterations, when the trace exceeds shared memory
 };
 struct FastConfig {
   int slots, threads, smem_bytes, grid;
   size_t table_bytes;
+  bool global_trace;  // iteration trace kept in global scratch (large I)
 };
 // Returns false when F is not supported by the fused kernel.
 bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg);

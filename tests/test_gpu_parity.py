@@ -305,3 +305,15 @@ def test_rfse_fp32_and_image_plan(fse):
                             precision="fp64", tile_dtype="f64")
     truth = np.stack([img[t:t + 16, l:l + 16] for _, t, l in blocks])
     assert abs(psnr_tiles(truth, np.clip(t64, 0, 255)) - psnr_tiles(truth, np.clip(tc, 0, 255))) < 1.0
+
+
+def test_fused_trace_beyond_shared_capacity(fse):
+    """I = 1200 > the 1056-entry shared trace of F = 64: the trace moves to
+    per-slot global scratch (Fig. 3 sweeps run to 2000 basis functions)."""
+    from paper_2204_14193_b200.synth import field
+    img = field(256, 256, seed=21).astype(np.float32)
+    blocks = np.array([[0, 64 * i + 16, 64 * j + 16] for i in range(4) for j in range(2)], np.int32)
+    tiles, get, plan = _run_plan(fse, img, blocks, 64, 16, 16, 1200)
+    assert plan.info["fast_path"] == 1
+    st = fp32_gate(img, blocks, tiles, get, 64, 16, 16, 0.8, 0.5, 1200, truth=_truth(img, blocks, 16))
+    print("I=1200", st)
