@@ -147,6 +147,7 @@ class Concealer:
         b = np.asarray(blocks, np.int32).reshape(-1, 3)
         order = np.argsort(b[:, 0], kind="stable")
         self.order = order
+        self.identity_order = bool(np.array_equal(order, np.arange(len(order))))
         b = b[order]
         self.n_frames, self.H, self.W, self.geometry = n_frames, H, W, geometry
         self.tile_dtype = tile_dtype
@@ -163,11 +164,15 @@ class Concealer:
         tdt = {"u8": torch.uint8, "f32": torch.float32, "f64": torch.float64}[tile_dtype]
         tt = torch.from_numpy(np.zeros((), self.frame_dtype)).dtype
         self.n_blocks = b.shape[0]
-        self.dev_frames = [torch.empty((chunk_frames, H, W), dtype=tt, device="cuda") for _ in range(2)]
+        self.nbuf = 4
+        self.dev_frames = [torch.empty((chunk_frames, H, W), dtype=tt, device="cuda")
+                           for _ in range(min(self.nbuf, len(self.chunks)))]
         self.dev_tiles = torch.empty((self.n_blocks, geometry.B, geometry.B), dtype=tdt, device="cuda")
         self.host_tiles = torch.empty_like(self.dev_tiles, device="cpu").pin_memory()
         self.copy_stream = torch.cuda.Stream()
-        self.compute_stream = torch.cuda.Stream()
+        # two compute streams: chunk k+1's persistent kernel fills the SMs
+        # freed by chunk k's tail instead of waiting for it
+        self.compute_streams = [torch.cuda.Stream(), torch.cuda.Stream()]
 
     @staticmethod
     def pin(frames: np.ndarray):
@@ -181,21 +186,25 @@ class Concealer:
     def d2h_bytes(self) -> int:
         return self.host_tiles.numel() * self.host_tiles.element_size()
 
-    def run(self, host_frames) -> np.ndarray:
+    def run(self, host_frames, copy: bool = False) -> np.ndarray:
         """host_frames: pinned torch tensor (n_frames, H, W).  Returns the
-        tiles in the caller's block order as a numpy array."""
+        tiles in the caller's block order.  When the caller's blocks are
+        already in frame order (the usual case) the result is a view of the
+        pinned tile buffer, valid until the next run (copy=True detaches it)."""
         import torch
 
-        cs, ks = self.copy_stream, self.compute_stream
-        done_compute = [None, None]
+        cs = self.copy_stream
+        nb = len(self.dev_frames)
+        done = [None] * len(self.chunks)  # compute-done event per chunk (frees its buffer)
         for i, (f0, f1, lo, hi, plan) in enumerate(self.chunks):
-            buf = self.dev_frames[i % 2]
+            buf = self.dev_frames[i % nb]
             with torch.cuda.stream(cs):
-                if done_compute[i % 2] is not None:
-                    cs.wait_event(done_compute[i % 2])  # buffer free again
+                if i >= nb:
+                    cs.wait_event(done[i - nb])  # the buffer's previous chunk has finished
                 buf[: f1 - f0].copy_(host_frames[f0:f1], non_blocking=True)
                 ready = torch.cuda.Event()
                 ready.record(cs)
+            ks = self.compute_streams[i % 2]
             with torch.cuda.stream(ks):
                 ks.wait_event(ready)
                 if plan is not None:
@@ -204,10 +213,14 @@ class Concealer:
                     self.host_tiles[lo:hi].copy_(self.dev_tiles[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(ks)
-                done_compute[i % 2] = ev
-        ks.synchronize()
-        out = np.empty(self.host_tiles.shape, self.host_tiles.numpy().dtype)
-        out[self.order] = self.host_tiles.numpy()
+                done[i] = ev
+        for ks in self.compute_streams:
+            ks.synchronize()
+        tiles = self.host_tiles.numpy()
+        if self.identity_order:
+            return tiles.copy() if copy else tiles
+        out = np.empty(tiles.shape, tiles.dtype)
+        out[self.order] = tiles
         return out
 
 
