@@ -33,10 +33,15 @@ namespace fse {
 
 template <int F> struct FG {
   static constexpr int LOG = F == 32 ? 5 : F == 64 ? 6 : 7;
-  static constexpr int NT = F * F / 32;   // threads per slot
+#ifndef FSE_BPT64
+#define FSE_BPT64 32
+#endif
+  static constexpr int BPT = F == 64 ? FSE_BPT64 : 32;  // spectrum bins per thread
+  static constexpr int NP = BPT / 2;      // SoA bin pairs per thread
+  static constexpr int NT = F * F / BPT;  // threads per slot
   static constexpr int NW = NT / 32;      // warps per slot
   static constexpr int CPL = F / 32;      // columns per lane
-  static constexpr int RPW = 32 / CPL;    // rows per warp
+  static constexpr int RPW = BPT / CPL;   // rows per warp
 #ifndef FSE_SLOTS64
 #define FSE_SLOTS64 5
 #endif
@@ -102,7 +107,7 @@ FSE_DEV float load_px(const void *frames, int dtype, size_t idx) {
 // row-major bin index of pair p, member mem (0 = a, 1 = b) for thread (w, lane)
 template <int F> FSE_DEV int bin_index(int w, int lane, int p, int mem) {
   if (F == 32) return (2 * p + mem) * 32 + lane;
-  if (F == 64) return (16 * w + p) * 64 + lane + 32 * mem;
+  if (F == 64) return (FG<64>::RPW * w + p) * 64 + lane + 32 * mem;
   return (8 * w + (p >> 1)) * 128 + lane + 64 * (p & 1) + 32 * mem;
 }
 
@@ -113,27 +118,34 @@ template <int F> FSE_DEV void decode_bin(int idx, int w, int &p, int &mem, int &
     p = row >> 1; mem = row & 1; lane = idx & 31;
   } else if (F == 64) {
     int row = idx >> 6;
-    p = row - 16 * w; mem = (idx >> 5) & 1; lane = idx & 31;
+    p = row - FG<64>::RPW * w; mem = (idx >> 5) & 1; lane = idx & 31;
   } else {
     int row = idx >> 7, c = idx & 127;
     p = 2 * (row - 8 * w) + (c >> 6); mem = (c >> 5) & 1; lane = c & 31;
   }
 }
 
-#define FSE_PICK(P)                           \
-  case P:                                     \
-    re = mem ? Rre[P].y : Rre[P].x;           \
-    im = mem ? Rim[P].y : Rim[P].x;           \
-    break;
+#define FSE_PICK(P)                                  \
+  case P:                                            \
+    if constexpr (P < NP - 1) {                      \
+      re = mem ? Rre[P].y : Rre[P].x;                \
+      im = mem ? Rim[P].y : Rim[P].x;                \
+      break;                                         \
+    }
 
 // Value of bin (pair p, member mem) of this thread; p is warp-uniform, so
-// the switch is a uniform branch, not a 16-way select chain.
-FSE_DEV void pick_bin(const float2 (&Rre)[16], const float2 (&Rim)[16], int p, int mem, float &re,
+// the switch is a uniform branch (BRX), not a select chain.  The last pair
+// is the default case (no range check).
+template <int NP>
+FSE_DEV void pick_bin(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p, int mem, float &re,
                       float &im) {
   switch (p) {
     FSE_PICK(0) FSE_PICK(1) FSE_PICK(2) FSE_PICK(3) FSE_PICK(4) FSE_PICK(5) FSE_PICK(6)
     FSE_PICK(7) FSE_PICK(8) FSE_PICK(9) FSE_PICK(10) FSE_PICK(11) FSE_PICK(12) FSE_PICK(13)
-    FSE_PICK(14) default: re = mem ? Rre[15].y : Rre[15].x; im = mem ? Rim[15].y : Rim[15].x; break;
+    FSE_PICK(14)
+    default:
+      re = mem ? Rre[NP - 1].y : Rre[NP - 1].x;
+      im = mem ? Rim[NP - 1].y : Rim[NP - 1].x;
   }
 }
 
@@ -318,7 +330,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
     const float *wtab = a.wtab + (size_t)cls * F * F;
     const size_t fbase = (size_t)fidx * (size_t)a.frame_stride;
     float e0p = 0.f;
-    float2 Rre[16], Rim[16];
+    float2 Rre[G::NP], Rim[G::NP];
     if constexpr (F == 128) {
       for (int i = st; i < F * F; i += G::NT) {
         const int m = i >> G::LOG, n = i & (F - 1);
@@ -337,7 +349,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
       slot_fft<F>(sp.scratch, fft_tw, st, slot);
       // R_w -> registers, exactly Hermitian
 #pragma unroll
-      for (int p = 0; p < 16; ++p) {
+      for (int p = 0; p < G::NP; ++p) {
         float2 xa, xb, ma, mb;
         {
           const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
@@ -448,7 +460,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         return make_float2(z.x, -z.y);
       };
 #pragma unroll
-      for (int p = 0; p < 16; ++p) {
+      for (int p = 0; p < G::NP; ++p) {
         const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
         const float2 xa = bin(ia >> G::LOG, ia & (F - 1)), xb = bin(ib >> G::LOG, ib & (F - 1));
         // an arithmetic op gives each SoA pair a fresh, aligned register
@@ -494,7 +506,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         int bp2 = 8;
 #endif
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
+        for (int p = 0; p < G::NP; ++p) {
           const float4 wv = tp[(F == 32 ? 2 * p : p) * F];
           const float2 wr = make_float2(wv.x, wv.y), wi = make_float2(wv.z, wv.w);
           ffma2_acc(Rre[p], wr, -cre);
@@ -526,7 +538,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
 #pragma unroll
         for (int h = 0; h < 4; ++h) co[h] = (lane + 32 * h - v) & (F - 1);
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
+        for (int p = 0; p < G::NP; ++p) {
           const int r = (rowoff + (p >> 1)) * F;
           const int q = 2 * (p & 1);
           const float2 wr = make_float2(Tre[r + co[q]], Tre[r + co[q + 1]]);
@@ -549,7 +561,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
       int pw, mw, ow;
       decode_bin<F>((int)widx, w, pw, mw, ow);
       float are, aim;
-      pick_bin(Rre, Rim, pw, mw, are, aim);
+      pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
       are = __shfl_sync(0xffffffffu, are, ow);
       aim = __shfl_sync(0xffffffffu, aim, ow);
       unsigned gidx = widx, gkey = wmax;
@@ -590,7 +602,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
     slot_sync<F>(slot);
 
     // ------------------------------------------------ synthesis + store
-    constexpr int PX = 2;  // (F/4)^2 / NT loss pixels per thread
+    constexpr int PX = (F / 4) * (F / 4) / G::NT;  // loss pixels per thread
     float g[PX];
     int pm[PX], pn[PX];
 #pragma unroll
