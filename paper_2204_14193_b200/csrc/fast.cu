@@ -36,7 +36,10 @@ template <int F> struct FG {
 #ifndef FSE_BPT64
 #define FSE_BPT64 32
 #endif
-  static constexpr int BPT = F == 64 ? FSE_BPT64 : 32;  // spectrum bins per thread
+#ifndef FSE_BPT128
+#define FSE_BPT128 32
+#endif
+  static constexpr int BPT = F == 64 ? FSE_BPT64 : F == 128 ? FSE_BPT128 : 32;  // bins per thread
   static constexpr int NP = BPT / 2;      // SoA bin pairs per thread
   static constexpr int NT = F * F / BPT;  // threads per slot
   static constexpr int NW = NT / 32;      // warps per slot
@@ -45,21 +48,23 @@ template <int F> struct FG {
 #ifndef FSE_SLOTS64
 #define FSE_SLOTS64 5
 #endif
-  static constexpr int S = F == 32 ? 16 : F == 64 ? FSE_SLOTS64 : 1;
+#ifndef FSE_SLOTS32
+#define FSE_SLOTS32 20
+#endif
+  static constexpr int S = F == 32 ? FSE_SLOTS32 : F == 64 ? FSE_SLOTS64 : 1;
   static constexpr int CTA = NT * S;      // threads per CTA
   static constexpr bool PLANAR = F == 128;  // planar re/im table (pair table would not fit)
-  static constexpr bool ALIAS = F == 128;   // FFT scratch and table share one region
   // rows of the row-extended table: the thread walks rows rowoff + step*p
-  static constexpr int TROWS = F == 32 ? F + 31 : F == 64 ? F + 15 : F + 7;
+  static constexpr int TROWS = F == 32 ? F + 31 : F == 64 ? F + 15 : F + RPW - 1;
   static constexpr size_t TABLE_BYTES =
       PLANAR ? (size_t)TROWS * F * 2 * sizeof(float) : (size_t)TROWS * F * sizeof(float4);
-  // FFT scratch: radix-2 in place (F = 128) or the real half-spectrum scheme
-  // (F <= 64: max(F/2 x (F+1), F x (F/2+1)) complex, padded rows)
-  static constexpr size_t SCRATCH =
-      F == 128 ? (size_t)F * F * sizeof(float2)
-               : (((size_t)F * (F / 2 + 1) * sizeof(float2) + 15) & ~(size_t)15);
-  static constexpr int TRACE_CAP = F == 128 ? 1 << 30 : (int)(SCRATCH / 16);
-  static constexpr size_t REGION = ALIAS ? (TABLE_BYTES > SCRATCH ? TABLE_BYTES : SCRATCH) : TABLE_BYTES;
+  // real half-spectrum FFT scratch: max(F/2 x (F+1), F x (F/2+1)) complex
+  static constexpr size_t SCRATCH = (((size_t)F * (F / 2 + 1) * sizeof(float2) + 15) & ~(size_t)15);
+  static constexpr int TRACE_CAP = (int)(SCRATCH / 16);
+  // the length-F FFTs of the setup: QT lanes per FFT, VPT values per lane
+  static constexpr int QT = F == 128 ? 8 : F / 8;
+  static constexpr int VPT = F / QT;
+  static constexpr size_t REGION = TABLE_BYTES;
 };
 
 FSE_DEV float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
@@ -108,7 +113,7 @@ FSE_DEV float load_px(const void *frames, int dtype, size_t idx) {
 template <int F> FSE_DEV int bin_index(int w, int lane, int p, int mem) {
   if (F == 32) return (2 * p + mem) * 32 + lane;
   if (F == 64) return (FG<64>::RPW * w + p) * 64 + lane + 32 * mem;
-  return (8 * w + (p >> 1)) * 128 + lane + 64 * (p & 1) + 32 * mem;
+  return (FG<128>::RPW * w + (p >> 1)) * 128 + lane + 64 * (p & 1) + 32 * mem;
 }
 
 // the pair index / member / owning lane of a bin owned by warp w (uniform)
@@ -121,7 +126,7 @@ template <int F> FSE_DEV void decode_bin(int idx, int w, int &p, int &mem, int &
     p = row - FG<64>::RPW * w; mem = (idx >> 5) & 1; lane = idx & 31;
   } else {
     int row = idx >> 7, c = idx & 127;
-    p = 2 * (row - 8 * w) + (c >> 6); mem = (c >> 5) & 1; lane = c & 31;
+    p = 2 * (row - FG<128>::RPW * w) + (c >> 6); mem = (c >> 5) & 1; lane = c & 31;
   }
 }
 
@@ -148,48 +153,6 @@ FSE_DEV void pick_bin(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p, i
       im = mem ? Rim[NP - 1].y : Rim[NP - 1].x;
   }
 }
-
-// In-place radix-2 DIT 2-D FFT of the slot's F x F scratch (input stored in
-// bit-reversed row and column order), forward kernel exp(-2 pi i / F).
-template <int F>
-FSE_DEV void slot_fft(float2 *S, const float2 *tw, int st, int slot) {
-  constexpr int HALF = F / 2;
-  // rows
-#pragma unroll 1
-  for (int lh = 0; lh < FG<F>::LOG; ++lh) {
-    const int half = 1 << lh;
-#pragma unroll 4
-    for (int t = st; t < F * HALF; t += FG<F>::NT) {
-      const int row = t / HALF, j = t - row * HALF;
-      const int k = j & (half - 1);
-      const int i0 = ((j >> lh) << (lh + 1)) + k, i1 = i0 + half;
-      const float2 w = tw[k << (FG<F>::LOG - 1 - lh)];
-      float2 a = S[row * F + i0], b = S[row * F + i1];
-      float2 x = make_float2(b.x * w.x - b.y * w.y, b.x * w.y + b.y * w.x);
-      S[row * F + i0] = make_float2(a.x + x.x, a.y + x.y);
-      S[row * F + i1] = make_float2(a.x - x.x, a.y - x.y);
-    }
-    slot_sync<F>(slot);
-  }
-  // columns (consecutive threads -> consecutive columns: conflict-free)
-#pragma unroll 1
-  for (int lh = 0; lh < FG<F>::LOG; ++lh) {
-    const int half = 1 << lh;
-#pragma unroll 4
-    for (int t = st; t < F * HALF; t += FG<F>::NT) {
-      const int col = t & (F - 1), j = t >> FG<F>::LOG;
-      const int k = j & (half - 1);
-      const int i0 = ((j >> lh) << (lh + 1)) + k, i1 = i0 + half;
-      const float2 w = tw[k << (FG<F>::LOG - 1 - lh)];
-      float2 a = S[i0 * F + col], b = S[i1 * F + col];
-      float2 x = make_float2(b.x * w.x - b.y * w.y, b.x * w.y + b.y * w.x);
-      S[i0 * F + col] = make_float2(a.x + x.x, a.y + x.y);
-      S[i1 * F + col] = make_float2(a.x - x.x, a.y - x.y);
-    }
-    slot_sync<F>(slot);
-  }
-}
-
 
 // ------------------------------------------------ radix-8 register FFT
 FSE_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
@@ -218,32 +181,69 @@ FSE_DEV void dft4(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
   x0 = cadd(a0, a1); x1 = cadd(a2, a3); x2 = csub(a0, a1); x3 = csub(a2, a3);
 }
 
-// Length-F forward FFT by a group of Q = F/8 lanes of one warp.  Lane t
-// holds x[t + Q k] (k < 8) in v; on return it holds X[q1 + 8 q2] for its
-// q1 set (Q = 8: q1 = t; Q = 4: q1 in {t, t+4}) in v[q2] (Q = 8) or
-// v[q2] (q1 = t) / v[4 + q2] (q1 = t + 4) for Q = 4.  `ex` is this group's
-// exchange area (8*Q complex, element (q1, t) at ex[q1 * Q + t]).
+// In-register forward DFT-16 (4 x 4), natural order in and out.
+FSE_DEV void dft16(float2 (&x)[16], const float2 *tw, int twstep) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) dft4(x[b], x[b + 4], x[b + 8], x[b + 12]);
+#pragma unroll
+  for (int b = 1; b < 4; ++b)
+#pragma unroll
+    for (int c = 1; c < 4; ++c) x[b + 4 * c] = cmul(x[b + 4 * c], tw[b * c * twstep]);
+  float2 y[16];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float2 a0 = x[4 * c], a1 = x[4 * c + 1], a2 = x[4 * c + 2], a3 = x[4 * c + 3];
+    dft4(a0, a1, a2, a3);
+    y[c] = a0; y[c + 4] = a1; y[c + 8] = a2; y[c + 12] = a3;
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = y[k];
+}
+
+// Length-F forward FFT by a group of QT lanes of one warp.  Lane t holds
+// x[t + QT k] (k < VPT) in v.  F = 32, 64: radix 8 x (F/8) (QT = F/8 lanes,
+// 8 values each); F = 128: radix 16 x 8 (8 lanes, 16 values each).  One
+// exchange through `ex` (element (q1, t) at ex[(q1 * QT + t) * es]); on
+// return v[i] holds X[group_out<F>(t, i)].
 template <int F>
-FSE_DEV void group_fft(float2 (&v)[8], float2 *ex, int es, const float2 *tw, int t) {
-  constexpr int Q = F / 8;
-  dft8(v);
+FSE_DEV void group_fft(float2 (&v)[FG<F>::VPT], float2 *ex, int es, const float2 *tw, int t) {
+  constexpr int QT = FG<F>::QT;
+  if constexpr (F == 128) {
+    dft16(v, tw, F / 16);
 #pragma unroll
-  for (int q1 = 1; q1 < 8; ++q1) v[q1] = cmul(v[q1], tw[t * q1]);
+    for (int q1 = 1; q1 < 16; ++q1) v[q1] = cmul(v[q1], tw[t * q1]);
 #pragma unroll
-  for (int q1 = 0; q1 < 8; ++q1) ex[(q1 * Q + t) * es] = v[q1];
-  __syncwarp();
-  if (Q == 8) {
+    for (int q1 = 0; q1 < 16; ++q1) ex[(q1 * QT + t) * es] = v[q1];
+    __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = ex[(t * Q + k) * es];
-    dft8(v);
-  } else {
+    for (int h = 0; h < 2; ++h) {
+      float2 y[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v[k] = ex[(t * Q + k) * es];
-      v[4 + k] = ex[((t + 4) * Q + k) * es];
+      for (int k = 0; k < 8; ++k) y[k] = ex[((t + 8 * h) * QT + k) * es];
+      dft8(y);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[8 * h + k] = y[k];
     }
-    dft4(v[0], v[1], v[2], v[3]);
-    dft4(v[4], v[5], v[6], v[7]);
+  } else {
+    dft8(v);
+#pragma unroll
+    for (int q1 = 1; q1 < 8; ++q1) v[q1] = cmul(v[q1], tw[t * q1]);
+#pragma unroll
+    for (int q1 = 0; q1 < 8; ++q1) ex[(q1 * QT + t) * es] = v[q1];
+    __syncwarp();
+    if (QT == 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = ex[(t * QT + k) * es];
+      dft8(v);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = ex[(t * QT + k) * es];
+        v[4 + k] = ex[((t + 4) * QT + k) * es];
+      }
+      dft4(v[0], v[1], v[2], v[3]);
+      dft4(v[4], v[5], v[6], v[7]);
+    }
   }
   __syncwarp();
 }
@@ -256,6 +256,7 @@ FSE_DEV void group_fft_idle() {
 
 // output index of v[i] after group_fft for lane t
 template <int F> FSE_DEV int group_out(int t, int i) {
+  if (F == 128) return (i < 8) ? t + 16 * i : (t + 8) + 16 * (i - 8);
   if (F == 64) return t + 8 * i;
   return (i < 4) ? t + 8 * i : (t + 4) + 8 * (i - 4);
 }
@@ -276,18 +277,17 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
   float2 *fft_tw = syn_tw + F;                     // exp(-2 pi i j / F), j < F
   char *slots_base = (char *)(fft_tw + F);
   const size_t slot_bytes =
-      (G::ALIAS ? 0 : G::SCRATCH) + 2 * G::NW * sizeof(uint4) + 64 +
-      (G::ALIAS ? (size_t)iter_cap * sizeof(float4) : 0);
+      G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64;
 
   const int tid = threadIdx.x;
   const int slot = tid / G::NT, st = tid - slot * G::NT;
   const int w = st >> 5, lane = st & 31;
   char *sb = slots_base + slot * slot_bytes;
   SlotPtrs<F> sp;
-  sp.scratch = G::ALIAS ? (float2 *)region : (float2 *)sb;
-  sp.xch = (uint4 *)(sb + (G::ALIAS ? 0 : G::SCRATCH));
+  sp.scratch = (float2 *)sb;
+  sp.xch = (uint4 *)(sb + G::SCRATCH);
   sp.red = (float *)(sp.xch + 2 * G::NW);
-  sp.trace = G::ALIAS ? (float4 *)((char *)sp.red + 64) : (float4 *)sp.scratch;
+  sp.trace = (float4 *)sp.scratch;  // the FFT scratch holds the trace after setup
   if (a.trace_scratch)  // more iterations than the shared trace holds: per-slot global scratch
     sp.trace = a.trace_scratch + ((size_t)blockIdx.x * G::S + slot) * a.iterations;
 
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
   bool first = true;
   for (int round = blockIdx.x; round < a.n_rounds; round += gridDim.x) {
     const int cls = __ldg(a.round_class + round);
-    if (!G::ALIAS && cls != loaded) {
+    if (cls != loaded) {
       __syncthreads();
       copy_table(region, (const char *)a.table + (size_t)cls * a.table_bytes, a.table_bytes, tid,
                  blockDim.x);
@@ -331,48 +331,18 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
     const size_t fbase = (size_t)fidx * (size_t)a.frame_stride;
     float e0p = 0.f;
     float2 Rre[G::NP], Rim[G::NP];
-    if constexpr (F == 128) {
-      for (int i = st; i < F * F; i += G::NT) {
-        const int m = i >> G::LOG, n = i & (F - 1);
-        const int y = wt + m, x = wl + n;
-        const float wv = __ldg(wtab + i);
-        float v = 0.f;
-        if (wv != 0.f && y >= 0 && y < a.H && x >= 0 && x < a.W) {
-          const float s = load_px(a.frames, a.dtype, fbase + (size_t)y * a.pitch + x);
-          v = s * wv;
-          e0p += v * s;
-        }
-        const int rm = __brev(m) >> (32 - G::LOG), rn = __brev(n) >> (32 - G::LOG);
-        sp.scratch[rm * F + rn] = make_float2(v, 0.f);
-      }
-      slot_sync<F>(slot);
-      slot_fft<F>(sp.scratch, fft_tw, st, slot);
-      // R_w -> registers, exactly Hermitian
-#pragma unroll
-      for (int p = 0; p < G::NP; ++p) {
-        float2 xa, xb, ma, mb;
-        {
-          const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
-          const int ra = ia >> G::LOG, ca = ia & (F - 1), rb = ib >> G::LOG, cb = ib & (F - 1);
-          xa = sp.scratch[ia];
-          xb = sp.scratch[ib];
-          ma = sp.scratch[((F - ra) & (F - 1)) * F + ((F - ca) & (F - 1))];
-          mb = sp.scratch[((F - rb) & (F - 1)) * F + ((F - cb) & (F - 1))];
-        }
-        Rre[p] = make_float2((xa.x + ma.x) * 0.5f, (xb.x + mb.x) * 0.5f);
-        Rim[p] = make_float2((xa.y - ma.y) * 0.5f, (xb.y - mb.y) * 0.5f);
-      }
-    } else {
-      // Real-input 2-D FFT, half spectrum (F in {32, 64}):
+    {
+      // Real-input 2-D FFT, half spectrum:
       //   rows   -- row pairs packed as one complex row, z_j = x_2j + i x_2j+1,
       //             one length-F FFT per pair (only pairs meeting the support);
       //   columns -- columns 1..F/2-1 of the untangled row spectra, plus
       //             columns 0 and F/2 packed as one complex column;
       //   the other half follows from X[k][l] = conj(X[-k][-l]), so R_w is
       //   exactly Hermitian by construction.
-      // Each length-F FFT is radix 8 x Q in registers of Q = F/8 lanes with
-      // one shared-memory exchange (group_fft).
-      constexpr int Q = F / 8, NG = G::NT / Q, H = F / 2, ZS = F + 1, XS = H + 1, CP = H / NG;
+      // Each length-F FFT runs in the registers of QT lanes (radix 8 x F/8,
+      // or 16 x 8 for F = 128) with one shared-memory exchange (group_fft).
+      constexpr int Q = G::QT, VPT = G::VPT, NG = G::NT / Q, H = F / 2, ZS = F + 1, XS = H + 1,
+                    CP = H / NG;
       const int g = st / Q, t = st - (st / Q) * Q;
       float2 *S = sp.scratch;
       const int4 rect = __ldg((const int4 *)a.support_rect + cls);  // (r0, c0, r1, c1)
@@ -385,10 +355,10 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
       for (int jb = j0; jb < j1; jb += NG) {
         const int j = jb + g;
         const bool act = j < j1;
-        float2 v[8];
+        float2 v[VPT];
         const int y0 = wt + 2 * j;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < VPT; ++k) {
           const int n = t + Q * k, x = wl + n;
           float xe = 0.f, xo = 0.f;
           if (act && x >= 0 && x < a.W) {
@@ -410,18 +380,18 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         if (act) {
           group_fft<F>(v, row, 1, fft_tw, t);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) row[group_out<F>(t, i)] = v[i];
+          for (int i = 0; i < VPT; ++i) row[group_out<F>(t, i)] = v[i];
         } else {
           group_fft_idle();
         }
       }
       slot_sync<F>(slot);
-      float2 cin[CP][8];
+      float2 cin[CP][VPT];
 #pragma unroll
       for (int pass = 0; pass < CP; ++pass) {
         const int c = g + pass * NG;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < VPT; ++k) {
           const int m = t + Q * k, j = m >> 1, odd = m & 1;
           float2 y = make_float2(0.f, 0.f);
           if (j >= j0 && j < j1) {
@@ -446,7 +416,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         const int c = g + pass * NG;
         group_fft<F>(cin[pass], S + c, XS, fft_tw, t);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) S[group_out<F>(t, i) * XS + c] = cin[pass][i];
+        for (int i = 0; i < VPT; ++i) S[group_out<F>(t, i) * XS + c] = cin[pass][i];
       }
       slot_sync<F>(slot);
       auto bin = [&](int r, int c) -> float2 {
@@ -478,11 +448,6 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
     if (st == 0)
       for (int k = 0; k < G::NW; ++k) e += sp.red[k];
 
-    if (G::ALIAS) {  // single slot: bring the class table into the region
-      copy_table(region, (const char *)a.table + (size_t)cls * a.table_bytes, a.table_bytes, tid,
-                 blockDim.x);
-      __syncthreads();
-    }
 
     // ------------------------------------------------------- iterations
     const float ginv = a.gamma * __ldg(a.inv_w00 + cls);
@@ -654,8 +619,8 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
 
 template <int F> static size_t fast_smem(int iter_cap) {
   typedef FG<F> G;
-  size_t slot_bytes = (G::ALIAS ? 0 : G::SCRATCH) + 2 * G::NW * sizeof(uint4) + 64 +
-                      (G::ALIAS ? (size_t)iter_cap * sizeof(float4) : 0);
+  (void)iter_cap;
+  size_t slot_bytes = G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64;
   return G::REGION + 2 * (size_t)F * sizeof(float2) + G::S * slot_bytes;
 }
 
@@ -672,9 +637,8 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
       smem = fast_smem<64>(0); tb = FG<64>::TABLE_BYTES; S = FG<64>::S;
       break;
     case 128:
-      cfg->global_trace = iterations > 2048;
-      smem = fast_smem<128>(cfg->global_trace ? 0 : iterations); tb = FG<128>::TABLE_BYTES;
-      S = FG<128>::S;
+      cfg->global_trace = iterations > FG<128>::TRACE_CAP;
+      smem = fast_smem<128>(0); tb = FG<128>::TABLE_BYTES; S = FG<128>::S;
       break;
     default:
       return false;
@@ -750,7 +714,7 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
   if (!a.fast_table) return;
   char *tab = (char *)a.fast_table + (size_t)c * a.fast_table_bytes;
   if (F == 128) {
-    const int TR = F + 7;
+    const int TR = FG<128>::TROWS;
     float *Tre = (float *)tab, *Tim = Tre + TR * F;
     for (int i = threadIdx.x; i < TR * F; i += blockDim.x) {
       const int r = i / F, q = i - r * F;
@@ -759,7 +723,7 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       Tim[i] = (float)x.y;
     }
   } else {
-    const int TR = F == 32 ? F + 31 : F + 15;
+    const int TR = F == 32 ? FG<32>::TROWS : FG<64>::TROWS;
     float4 *T4 = (float4 *)tab;
     for (int i = threadIdx.x; i < TR * F; i += blockDim.x) {
       const int r = i / F, q = i - r * F;
