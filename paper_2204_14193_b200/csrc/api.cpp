@@ -442,6 +442,7 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     fse::FastArgs a{};
     a.F = p->F; a.B = p->B; a.border = p->border; a.iterations = p->iterations;
     a.gamma = (float)p->gamma; a.n_rounds = p->n_rounds; a.rounds = p->rounds;
+    a.n_blocks = p->n_blocks; a.n_classes = p->n_classes;
     a.round_class = p->round_class; a.blocks = p->blocks; a.wtab = p->wtab; a.table = p->table;
     a.table_bytes = p->cfg.table_bytes; a.inv_w00 = p->inv_w00; a.support_rect = p->rects;
     a.frames = frames; a.dtype = dtype; a.pitch = pitch; a.frame_stride = frame_stride;

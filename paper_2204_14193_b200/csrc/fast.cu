@@ -67,6 +67,16 @@ template <int F> struct FG {
   static constexpr size_t REGION = TABLE_BYTES;
 };
 
+// FSE_CHECKS builds (tests only): device-side bounds checks on every shared
+// and global index of the fused kernel (compute-sanitizer is not available
+// on this pool).
+#ifdef FSE_CHECKS
+#include <cassert>
+#define FSE_CHECK(cond) assert(cond)
+#else
+#define FSE_CHECK(cond) ((void)0)
+#endif
+
 FSE_DEV float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 // acc = a * b + acc with the accumulator as a read-write PTX operand.  With
 // the intrinsic form ptxas writes the result into the (dead) W' register
@@ -324,6 +334,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
     if (b < 0) continue;
 
     // ---------------------------------------------------------- load s*w
+    FSE_CHECK(b < a.n_blocks && cls < a.n_classes);
     const int fidx = __ldg(a.blocks + 3 * b), top = __ldg(a.blocks + 3 * b + 1),
               left = __ldg(a.blocks + 3 * b + 2);
     const int wt = top - off, wl = left - off;
@@ -380,7 +391,10 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         if (act) {
           group_fft<F>(v, row, 1, fft_tw, t);
 #pragma unroll
-          for (int i = 0; i < VPT; ++i) row[group_out<F>(t, i)] = v[i];
+          for (int i = 0; i < VPT; ++i) {
+            FSE_CHECK(j * ZS + group_out<F>(t, i) < (int)(G::SCRATCH / sizeof(float2)));
+            row[group_out<F>(t, i)] = v[i];
+          }
         } else {
           group_fft_idle();
         }
@@ -416,7 +430,10 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         const int c = g + pass * NG;
         group_fft<F>(cin[pass], S + c, XS, fft_tw, t);
 #pragma unroll
-        for (int i = 0; i < VPT; ++i) S[group_out<F>(t, i) * XS + c] = cin[pass][i];
+        for (int i = 0; i < VPT; ++i) {
+          FSE_CHECK(group_out<F>(t, i) * XS + c < (int)(G::SCRATCH / sizeof(float2)));
+          S[group_out<F>(t, i) * XS + c] = cin[pass][i];
+        }
       }
       slot_sync<F>(slot);
       auto bin = [&](int r, int c) -> float2 {
@@ -472,6 +489,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
 #endif
 #pragma unroll
         for (int p = 0; p < G::NP; ++p) {
+          FSE_CHECK(rowoff + (F == 32 ? 2 * p : p) < G::TROWS);
           const float4 wv = tp[(F == 32 ? 2 * p : p) * F];
           const float2 wr = make_float2(wv.x, wv.y), wi = make_float2(wv.z, wv.w);
           ffma2_acc(Rre[p], wr, -cre);
@@ -506,6 +524,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         for (int p = 0; p < G::NP; ++p) {
           const int r = (rowoff + (p >> 1)) * F;
           const int q = 2 * (p & 1);
+          FSE_CHECK(rowoff + (p >> 1) < G::TROWS);
           const float2 wr = make_float2(Tre[r + co[q]], Tre[r + co[q + 1]]);
           const float2 wi = make_float2(Tim[r + co[q]], Tim[r + co[q + 1]]);
           ffma2_acc(Rre[p], wr, -cre);
@@ -552,6 +571,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
       cim = ginv * aim;
       if (st == 0) {
         e -= dinv * (are * are + aim * aim);
+        FSE_CHECK(a.trace_scratch || it < G::TRACE_CAP);
         sp.trace[it] = make_float4(__uint_as_float((unsigned)u | ((unsigned)v << 16)), cre, cim, e);
         if (a.trace_uv) {
           const size_t o = (size_t)b * a.iterations + it;
@@ -605,6 +625,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
 #pragma unroll
     for (int k = 0; k < PX; ++k) {
       const size_t o = (size_t)b * a.B * a.B + (size_t)(pm[k] - off) * a.B + (pn[k] - off);
+      FSE_CHECK(pm[k] - off < a.B && pn[k] - off < a.B && b < a.n_blocks);
       if (a.tile_dtype == 0) {
         ((uint8_t *)a.tiles)[o] = (uint8_t)__float2int_rn(fminf(fmaxf(g[k], 0.f), 255.f));
       } else if (a.tile_dtype == 1) {

@@ -66,7 +66,7 @@ cudaError_t launch_class_setup(const ClassSetupArgs &a, cudaStream_t s);
 struct FastArgs {
   int F, B, border, iterations;
   float gamma;
-  int n_rounds;
+  int n_rounds, n_blocks, n_classes;
   const int32_t *rounds;       // n_rounds x slots block ids (-1 = idle)
   const int32_t *round_class;  // n_rounds
   const int32_t *blocks;       // n_blocks x 3 (frame, top, left)
