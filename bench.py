@@ -57,7 +57,8 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed
+    region (one `nvidia-smi -lms` process, started before and stopped after)."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -66,41 +67,56 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.15)  # let the first samples land before the timed region
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is None:
+            return
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        self.samples = [[x.strip() for x in l.split(",")] for l in out.splitlines() if l.strip()]
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        num = lambda x: x.replace(".", "", 1).isdigit()
+        sm = [float(s[0]) for s in self.samples if num(s[0])]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and num(s[1])]
+        # under load = samples above idle clocks
+        load = [x for x in sm if x > 0.5 * max(sm)] if sm else []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 4 + i and s[4 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
+        return {"sm_mhz": statistics.median(load) if load else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.samples)}
+
+
+def measured_ceilings():
+    """Shared-memory ceilings measured on this pool's B200s by scripts/smem_peak.cu."""
+    try:
+        rows = [json.loads(l) for l in open(os.path.join(REPO, "profiles", "r01", "smem_peak.jsonl"))]
+        pick = lambda t: max(r["smem_TBps"] for r in rows if r["test"] == t and r.get("threads") == 640)
+        return {"lds128_TBps": pick("lds128"), "loop_mix_TBps": pick("lds128+6ffma2+argmax"),
+                "source": "profiles/r01/smem_peak.jsonl (scripts/smem_peak.cu)"}
+    except Exception:
+        return None
 
 
 def measured_peaks():
@@ -301,6 +317,7 @@ def main():
     peak_fp32 = sms * 128 * 2 * sm_max * 1e6 / 1e12
     clocks = clk.summary()
     traffic = ncu_traffic(f"config{a.config}")
+    ceil = measured_ceilings()
     line = {
         "metric": "lost_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
@@ -321,6 +338,9 @@ def main():
                      "fp32_peak_tflops": peak_fp32,
                      "frac_at_observed_clock": (achieved / (sms * 128 * clocks["sm_mhz"] * 1e6 / 1e12))
                      if clocks.get("sm_mhz") else None,
+                     "measured_ceilings": ceil,
+                     "frac_of_measured_lds128": achieved / ceil["lds128_TBps"] if ceil else None,
+                     "frac_of_loop_mix_ceiling": achieved / ceil["loop_mix_TBps"] if ceil else None,
                      "kernel_ms": statistics.mean(kern_ms)},
         "clocks": clocks,
         "gpu_launches": a.steps,
