@@ -152,8 +152,9 @@ def cmd_sweep(a):
     for bf in [int(x) for x in a.bf_counts.split(",") if x]:
         tiles, dt = _conceal_once(img, pattern, a, bf)
         rows += _report_rows(a.algo, bf, img, pattern, tiles, dt, a.block)
-    sys.stdout.write(_write_csv(a.report, ["algo", "bf_count", "block_index", "psnr_db", "sec_per_block"],
-                                [r for r in rows if r[2] == "pooled"] if not a.report else rows))
+    hdr = ["algo", "bf_count", "block_index", "psnr_db", "sec_per_block"]
+    _write_csv(a.report, hdr, rows)  # full per-block report
+    sys.stdout.write(_write_csv(None, hdr, [r for r in rows if r[2] == "pooled"]))
     return 0
 
 

@@ -71,3 +71,31 @@ def test_cli_conceal_run(tmp_path, cuda_ok):
     assert rows[-1][2] == "pooled" and 10 < float(rows[-1][3]) < 60
     assert (pgm.load_image(dmg)[mask] == 0).all()
     assert cli.main(["selfcheck"]) == 0
+
+
+@pytest.mark.gpu
+def test_cli_sweep_determinism_and_quality(tmp_path, cuda_ok):
+    """SPEC acceptance 5 (rFSE/cFSE pooled PSNR within 0.3 dB at >= 100 basis
+    functions, PSNR@200 >= PSNR@20), 6 (golden regression: same PSNR run to
+    run) and 8 (byte-identical outputs for identical flags and seed)."""
+    from paper_2204_14193_b200.synth import frame_u8
+    img = frame_u8(256, 256, seed=12)
+    src = str(tmp_path / "in.pgm")
+    pgm.save_image(img, src)
+    pooled = {}
+    for algo in ("cfse", "rfse"):
+        rep = str(tmp_path / f"{algo}.csv")
+        assert cli.main(["sweep", "--input", src, "--algo", algo, "--bf-counts", "20,100,200",
+                         "--report", rep, "--precision", "fp64"]) == 0
+        rows = [r for r in csv.reader(open(rep)) if r and r[2] == "pooled"]
+        pooled[algo] = {int(r[1]): float(r[3]) for r in rows}
+    assert pooled["cfse"][200] >= pooled["cfse"][20]
+    assert abs(pooled["cfse"][100] - pooled["rfse"][100]) <= 0.3
+    assert abs(pooled["cfse"][200] - pooled["rfse"][200]) <= 0.3
+    outs = []
+    for k in range(2):
+        out = str(tmp_path / f"o{k}.pgm")
+        assert cli.main(["conceal", "--input", src, "--output", out, "--iters", "100",
+                         "--precision", "fp32"]) == 0
+        outs.append(open(out, "rb").read())
+    assert outs[0] == outs[1]
