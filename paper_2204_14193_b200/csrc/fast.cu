@@ -142,25 +142,24 @@ template <int F> FSE_DEV void decode_bin(int idx, int w, int &p, int &mem, int &
 
 #define FSE_PICK(P)                                  \
   case P:                                            \
-    if constexpr (P < NP - 1) {                      \
+    if constexpr (P < NP) {                          \
       re = mem ? Rre[P].y : Rre[P].x;                \
       im = mem ? Rim[P].y : Rim[P].x;                \
-      break;                                         \
-    }
+    }                                                \
+    break;
 
 // Value of bin (pair p, member mem) of this thread; p is warp-uniform, so
-// the switch is a uniform branch (BRX), not a select chain.  The last pair
-// is the default case (no range check).
+// the switch is a uniform indirect branch (one BRX jump table: every case
+// present, p < NP promised), not a select chain.
 template <int NP>
 FSE_DEV void pick_bin(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p, int mem, float &re,
                       float &im) {
   switch (p) {
     FSE_PICK(0) FSE_PICK(1) FSE_PICK(2) FSE_PICK(3) FSE_PICK(4) FSE_PICK(5) FSE_PICK(6)
     FSE_PICK(7) FSE_PICK(8) FSE_PICK(9) FSE_PICK(10) FSE_PICK(11) FSE_PICK(12) FSE_PICK(13)
-    FSE_PICK(14)
+    FSE_PICK(14) FSE_PICK(15)
     default:
-      re = mem ? Rre[NP - 1].y : Rre[NP - 1].x;
-      im = mem ? Rim[NP - 1].y : Rim[NP - 1].x;
+      __builtin_unreachable();
   }
 }
 
