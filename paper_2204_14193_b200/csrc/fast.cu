@@ -25,6 +25,8 @@
 //   F=32 : a = (2p, lane),            b = (2p+1, lane)
 //   F=64 : a = (16w+p, lane),         b = (16w+p, lane+32)
 //   F=128: a = (8w+p/2, lane+64(p&1)), b = a + (0, 32)
+#include <string.h>
+
 #include "common.cuh"
 #include "dft.cuh"
 #include "kernels.h"
@@ -61,6 +63,8 @@ template <int F> struct FG {
   // real half-spectrum FFT scratch: max(F/2 x (F+1), F x (F/2+1)) complex
   static constexpr size_t SCRATCH = (((size_t)F * (F / 2 + 1) * sizeof(float2) + 15) & ~(size_t)15);
   static constexpr int TRACE_CAP = (int)(SCRATCH / 16);
+  // TMA window bytes (u8 support box: 32x24, 48x48, 64x64 at the configs)
+  static constexpr size_t STAGE = F == 32 ? 1024 : F == 64 ? 2560 : 4096;
   // the length-F FFTs of the setup: QT lanes per FFT, VPT values per lane
   static constexpr int QT = F == 128 ? 8 : F / 8;
   static constexpr int VPT = F / QT;
@@ -108,6 +112,34 @@ template <int F> FSE_DEV void slot_sync(int slot) {
   } else {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(FG<F>::NT) : "memory");
   }
+}
+
+// ----------------------------------------------------- TMA + mbarrier
+FSE_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+FSE_DEV void mbar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+// one thread: expect `bytes` and start the 3-D tile load (OOB elements -> 0)
+FSE_DEV void tma_window(void *dst, const CUtensorMap *map, uint64_t *bar, unsigned bytes, int x, int y,
+                        int z) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+FSE_DEV void mbar_wait(uint64_t *bar, int phase) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
 }
 
 FSE_DEV float load_px(const void *frames, int dtype, size_t idx) {
@@ -277,25 +309,36 @@ FSE_DEV void copy_table(void *dst, const void *src, size_t bytes, int tid, int n
   for (size_t i = tid; i < bytes / 16; i += nthr) d[i] = __ldg(s + i);
 }
 
-template <int F>
-__global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int iter_cap) {
+// TMA = true: u8 frames, each block's support window staged in shared memory
+// by a tensor-map load prefetched during the slot's previous block; TMA =
+// false: direct bounds-checked loads.  Separate instantiations keep each
+// variant's registers for its own path.
+template <int F, bool TMA>
+__global__ void __launch_bounds__(FG<F>::CTA, 1)
+    fast_kernel(FastArgs a, int iter_cap, const __grid_constant__ CUtensorMap tmap) {
   typedef FG<F> G;
   extern __shared__ __align__(16) char smem[];
   char *region = smem;
   float2 *syn_tw = (float2 *)(smem + G::REGION);  // exp(+2 pi i j / F), j < F
   float2 *fft_tw = syn_tw + F;                     // exp(-2 pi i j / F), j < F
-  char *slots_base = (char *)(fft_tw + F);
+  // slot regions 128-byte aligned for TMA destinations
+  char *slots_base = TMA ? (char *)(((uintptr_t)(fft_tw + F) + 127) & ~(uintptr_t)127)
+                         : (char *)(fft_tw + F);
+  constexpr size_t STG = TMA ? G::STAGE : 0;  // the direct-load variant keeps no staging area
   const size_t slot_bytes =
-      G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64;
+      TMA ? (STG + G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64 + 16 + 127) & ~(size_t)127
+          : G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64;
 
   const int tid = threadIdx.x;
   const int slot = tid / G::NT, st = tid - slot * G::NT;
   const int w = st >> 5, lane = st & 31;
   char *sb = slots_base + slot * slot_bytes;
   SlotPtrs<F> sp;
-  sp.scratch = (float2 *)sb;
-  sp.xch = (uint4 *)(sb + G::SCRATCH);
+  sp.scratch = (float2 *)(sb + STG);
+  sp.xch = (uint4 *)(sb + STG + G::SCRATCH);
   sp.red = (float *)(sp.xch + 2 * G::NW);
+  uint64_t *const mbar = (uint64_t *)((char *)sp.red + 64);  // TMA completion barrier
+  int *const tphase = (int *)(mbar + 1);                      // its expected phase
   sp.trace = (float4 *)sp.scratch;  // the FFT scratch holds the trace after setup
   if (a.trace_scratch)  // more iterations than the shared trace holds: per-slot global scratch
     sp.trace = a.trace_scratch + ((size_t)blockIdx.x * G::S + slot) * a.iterations;
@@ -306,7 +349,25 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
     syn_tw[j] = make_float2((float)c, (float)s);
     fft_tw[j] = make_float2((float)c, (float)-s);
   }
+  if constexpr (TMA) {
+    if (st == 0) {
+      mbar_init(mbar);
+      *tphase = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  // issue the TMA load of the support window of this slot's block in round rnd
+  auto prefetch = [&](int rnd) {
+    if constexpr (!TMA) return;
+    if (st != 0 || rnd >= a.n_rounds) return;
+    const int nb = __ldg(a.rounds + (size_t)rnd * G::S + slot);
+    if (nb < 0) return;
+    const int o = (F - a.B) / 2 - a.box_off;  // image offset of the box from the block
+    tma_window(sb, &tmap, mbar, (unsigned)(a.box_w * a.box_h), __ldg(a.blocks + 3 * nb + 2) - o,
+               __ldg(a.blocks + 3 * nb + 1) - o, __ldg(a.blocks + 3 * nb));
+  };
+  prefetch(blockIdx.x);
 
   const int off = (F - a.B) / 2;
   int loaded = -1;
@@ -329,8 +390,11 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
       if (a.stagger_ns > 0 && slot > 0) __nanosleep((unsigned)(slot * a.stagger_ns));
     }
     const int b = __ldg(a.rounds + (size_t)round * G::S + slot);
-    if (G::S == 1 && b < 0) continue;  // uniform for a single slot
-    if (b < 0) continue;
+    if (b < 0) {  // idle this round: keep the slot's prefetch chain going
+      if constexpr (TMA) prefetch(round + gridDim.x);
+      continue;
+    }
+    if constexpr (TMA) mbar_wait(mbar, *tphase);
 
     // ---------------------------------------------------------- load s*w
     FSE_CHECK(b < a.n_blocks && cls < a.n_classes);
@@ -367,24 +431,48 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         const bool act = j < j1;
         float2 v[VPT];
         const int y0 = wt + 2 * j;
+        if constexpr (TMA) {
+          // support window staged by TMA (zeros outside the image)
+          const uint8_t *stage = (const uint8_t *)sb;
+          const int br = 2 * j - a.box_off;
 #pragma unroll
-        for (int k = 0; k < VPT; ++k) {
-          const int n = t + Q * k, x = wl + n;
-          float xe = 0.f, xo = 0.f;
-          if (act && x >= 0 && x < a.W) {
-            const float we = __ldg(wtab + (2 * j) * F + n), wo = __ldg(wtab + (2 * j + 1) * F + n);
-            if (we != 0.f && y0 >= 0 && y0 < a.H) {
-              const float s = load_px(a.frames, a.dtype, fbase + (size_t)y0 * a.pitch + x);
-              xe = s * we;
-              e0p += xe * s;
+          for (int k = 0; k < VPT; ++k) {
+            const int n = t + Q * k, bc = n - a.box_off;
+            float xe = 0.f, xo = 0.f;
+            if (act && (unsigned)bc < (unsigned)a.box_w) {
+              if ((unsigned)br < (unsigned)a.box_h) {
+                const float s = (float)stage[br * a.box_w + bc];
+                xe = s * __ldg(wtab + (2 * j) * F + n);
+                e0p += xe * s;
+              }
+              if ((unsigned)(br + 1) < (unsigned)a.box_h) {
+                const float s = (float)stage[(br + 1) * a.box_w + bc];
+                xo = s * __ldg(wtab + (2 * j + 1) * F + n);
+                e0p += xo * s;
+              }
             }
-            if (wo != 0.f && y0 + 1 >= 0 && y0 + 1 < a.H) {
-              const float s = load_px(a.frames, a.dtype, fbase + (size_t)(y0 + 1) * a.pitch + x);
-              xo = s * wo;
-              e0p += xo * s;
-            }
+            v[k] = make_float2(xe, xo);
           }
-          v[k] = make_float2(xe, xo);
+        } else {
+#pragma unroll
+          for (int k = 0; k < VPT; ++k) {
+            const int n = t + Q * k, x = wl + n;
+            float xe = 0.f, xo = 0.f;
+            if (act && x >= 0 && x < a.W) {
+              const float we = __ldg(wtab + (2 * j) * F + n), wo = __ldg(wtab + (2 * j + 1) * F + n);
+              if (we != 0.f && y0 >= 0 && y0 < a.H) {
+                const float s = load_px(a.frames, a.dtype, fbase + (size_t)y0 * a.pitch + x);
+                xe = s * we;
+                e0p += xe * s;
+              }
+              if (wo != 0.f && y0 + 1 >= 0 && y0 + 1 < a.H) {
+                const float s = load_px(a.frames, a.dtype, fbase + (size_t)(y0 + 1) * a.pitch + x);
+                xo = s * wo;
+                e0p += xo * s;
+              }
+            }
+            v[k] = make_float2(xe, xo);
+          }
         }
         float2 *row = S + j * ZS;
         if (act) {
@@ -399,6 +487,10 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
         }
       }
       slot_sync<F>(slot);
+      if constexpr (TMA) {
+        if (st == 0) *tphase ^= 1;  // every thread of the slot has waited
+        prefetch(round + gridDim.x);  // the staged window has been consumed
+      }
       float2 cin[CP][VPT];
 #pragma unroll
       for (int pass = 0; pass < CP; ++pass) {
@@ -640,8 +732,9 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1) fast_kernel(FastArgs a, int ite
 template <int F> static size_t fast_smem(int iter_cap) {
   typedef FG<F> G;
   (void)iter_cap;
-  size_t slot_bytes = G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64;
-  return G::REGION + 2 * (size_t)F * sizeof(float2) + G::S * slot_bytes;
+  size_t slot_bytes =
+      (G::STAGE + G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64 + 16 + 127) & ~(size_t)127;
+  return G::REGION + 2 * (size_t)F * sizeof(float2) + 128 + G::S * slot_bytes;
 }
 
 bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
@@ -673,24 +766,31 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
 }
 
 template <int F> static cudaError_t launch_fast_t(const FastArgs &a, const FastConfig &cfg,
-                                                 cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(fast_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 const CUtensorMap *tmap, cudaStream_t s) {
+  auto kern = tmap ? fast_kernel<F, true> : fast_kernel<F, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        cfg.smem_bytes);
   if (e != cudaSuccess) return e;
   int grid = cfg.grid < a.n_rounds ? cfg.grid : a.n_rounds;
   if (grid <= 0) return cudaSuccess;
-  fast_kernel<F><<<grid, cfg.threads, cfg.smem_bytes, s>>>(
-      a, (F == 128 && !a.trace_scratch) ? a.iterations : 0);
+  CUtensorMap none;
+  memset(&none, 0, sizeof none);
+  kern<<<grid, cfg.threads, cfg.smem_bytes, s>>>(a, 0, tmap ? *tmap : none);
   return cudaGetLastError();
 }
 
-cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, cudaStream_t s) {
+cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap,
+                        cudaStream_t s) {
   switch (a.F) {
-    case 32: return launch_fast_t<32>(a, cfg, s);
-    case 64: return launch_fast_t<64>(a, cfg, s);
-    case 128: return launch_fast_t<128>(a, cfg, s);
+    case 32: return launch_fast_t<32>(a, cfg, tmap, s);
+    case 64: return launch_fast_t<64>(a, cfg, tmap, s);
+    case 128: return launch_fast_t<128>(a, cfg, tmap, s);
   }
   return cudaErrorInvalidValue;
+}
+
+size_t fast_stage_bytes(int F) {
+  return F == 32 ? FG<32>::STAGE : F == 64 ? FG<64>::STAGE : F == 128 ? FG<128>::STAGE : 0;
 }
 
 // ---------------------------------------------------------- class setup

@@ -1,6 +1,7 @@
 // kernels.h -- host-side launchers implemented in the .cu files and used by
 // the C-ABI layer (api.cpp).  Internal; not part of the public ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -85,6 +86,9 @@ struct FastArgs {
   float *trace_c, *trace_e;
   int stagger_ns;  // start offset per slot (desynchronises the slots' reduction phases)
   float4 *trace_scratch;  // grid x slots x iterations, when the trace exceeds shared memory
+  // TMA staging of the support window (u8 frames): box_w x box_h bytes at
+  // window offset (box_off, box_off); 0 = direct loads
+  int use_tma, box_w, box_h, box_off;
 };
 struct FastConfig {
   int slots, threads, smem_bytes, grid;
@@ -93,7 +97,10 @@ struct FastConfig {
 };
 // Returns false when F is not supported by the fused kernel.
 bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg);
-cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, cudaStream_t s);
+cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap,
+                        cudaStream_t s);
+// staging capacity (bytes per slot) of the TMA window for window size F
+size_t fast_stage_bytes(int F);
 
 // ------------------------------------------------------------- image f64
 // Gather F x F windows (f64, zero outside the image) for a list of blocks.

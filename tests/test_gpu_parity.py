@@ -317,3 +317,24 @@ def test_fused_trace_beyond_shared_capacity(fse):
     assert plan.info["fast_path"] == 1
     st = fp32_gate(img, blocks, tiles, get, 64, 16, 16, 0.8, 0.5, 1200, truth=_truth(img, blocks, 16))
     print("I=1200", st)
+
+
+def test_tma_window_staging_variant(fse):
+    """The opt-in TMA variant (FSE_TMA=1: tensor-map tile loads of each
+    block's support window, OOB zero fill at the image border) gives the same
+    tiles as the direct-load kernel."""
+    import os
+    import torch
+    from paper_2204_14193_b200.synth import frame_u8
+    frames = np.stack([frame_u8(270, 480, seed=70 + f) for f in range(3)])
+    blocks = fse.frames_pattern(3, 270, 480, 16, 0.08, seed=9)
+    blocks = np.concatenate([blocks, np.array([[0, 0, 0], [2, 256, 464]], np.int32)])
+    fr = torch.from_numpy(frames).cuda()
+    plan = fse.ConcealPlan(blocks, 270, 480, iterations=100)
+    direct = plan.run(fr, tile_dtype="f32").cpu().numpy()
+    os.environ["FSE_TMA"] = "1"
+    try:
+        staged = plan.run(fr, tile_dtype="f32").cpu().numpy()
+    finally:
+        del os.environ["FSE_TMA"]
+    assert np.array_equal(direct, staged)
