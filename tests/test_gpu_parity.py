@@ -328,7 +328,7 @@ def test_tma_window_staging_variant(fse):
     from paper_2204_14193_b200.synth import frame_u8
     frames = np.stack([frame_u8(270, 480, seed=70 + f) for f in range(3)])
     blocks = fse.frames_pattern(3, 270, 480, 16, 0.08, seed=9)
-    blocks = np.concatenate([blocks, np.array([[0, 0, 0], [2, 256, 464]], np.int32)])
+    blocks = np.concatenate([blocks, np.array([[0, 0, 0], [2, 254, 464]], np.int32)])
     fr = torch.from_numpy(frames).cuda()
     plan = fse.ConcealPlan(blocks, 270, 480, iterations=100)
     direct = plan.run(fr, tile_dtype="f32").cpu().numpy()
