@@ -74,11 +74,6 @@ int sm_count() {
   return n;
 }
 
-struct DevBuf {
-  void *p = nullptr;
-  ~DevBuf() { if (p) cudaFree(p); }
-};
-
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
 // libcuda link dependency)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -105,7 +100,6 @@ struct fse_plan {
   double rho = 0, gamma = 0;
   int n_classes = 0, n_rounds = 0;
   bool fast = false;
-  int stagger_ns = 0;
   fse::FastConfig cfg{};
   // device
   int32_t *blocks = nullptr, *rounds = nullptr, *round_class = nullptr, *block_class = nullptr;
@@ -190,9 +184,6 @@ int fse_extrapolate(int count, int M, int N, int precision, const double *signal
   if (count <= 0) return FSE_OK;
   if (!signal || !labels || !recon || !status || (iterations > 0 && (!us || !vs || !cs || !es)))
     return fail(FSE_ERR_VALUE, "null pointer");
-  // trace buffers must exist even for iterations == 0 (kernel indexes them)
-  int64_t dummy_i[2];
-  (void)dummy_i;
   const int chunk = 2048;
   for (int c0 = 0; c0 < count; c0 += chunk) {
     int n = std::min(chunk, count - c0);
@@ -367,7 +358,6 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
   if (p->fast) CK(p->alloc((char **)&p->table, (size_t)nc * p->cfg.table_bytes));
   if (p->fast && p->cfg.global_trace)
     CK(p->alloc(&p->trace_scratch, (size_t)p->cfg.grid * p->cfg.slots * iterations));
-  if (const char *e = getenv("FSE_STAGGER_NS")) p->stagger_ns = atoi(e);
 
   fse::ClassSetupArgs ca{};
   ca.n_classes = nc; ca.F = F; ca.rho = rho; ca.labels = p->labels; ca.W64 = p->W64;
@@ -468,7 +458,6 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.frames = frames; a.dtype = dtype; a.pitch = pitch; a.frame_stride = frame_stride;
     a.H = p->H; a.W = p->W; a.tiles = tiles; a.tile_dtype = tile_dtype;
     a.trace_uv = trace_uv; a.trace_c = (float *)trace_c; a.trace_e = (float *)trace_e;
-    a.stagger_ns = p->stagger_ns;
     a.trace_scratch = p->trace_scratch;
     // Optional TMA staging of each block's support window (u8 frames, opt-in
     // with FSE_TMA=1): one 3-D tile load per block, prefetched during the

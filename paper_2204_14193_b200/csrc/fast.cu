@@ -371,7 +371,6 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
 
   const int off = (F - a.B) / 2;
   int loaded = -1;
-  bool first = true;
   for (int round = blockIdx.x; round < a.n_rounds; round += gridDim.x) {
     const int cls = __ldg(a.round_class + round);
     if (cls != loaded) {
@@ -380,14 +379,6 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
                  blockDim.x);
       __syncthreads();
       loaded = cls;
-    }
-    if (first) {
-      // The slots of a CTA do identical work; started together (the table
-      // load above is a CTA barrier) they stay in lock-step, so their
-      // setup and reduction phases coincide.  Offsetting their start lets
-      // one slot's latency-bound phases overlap another's throughput work.
-      first = false;
-      if (a.stagger_ns > 0 && slot > 0) __nanosleep((unsigned)(slot * a.stagger_ns));
     }
     const int b = __ldg(a.rounds + (size_t)round * G::S + slot);
     if (b < 0) {  // idle this round: keep the slot's prefetch chain going

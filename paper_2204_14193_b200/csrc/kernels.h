@@ -84,7 +84,6 @@ struct FastArgs {
   int tile_dtype;
   int32_t *trace_uv;
   float *trace_c, *trace_e;
-  int stagger_ns;  // start offset per slot (desynchronises the slots' reduction phases)
   float4 *trace_scratch;  // grid x slots x iterations, when the trace exceeds shared memory
   // TMA staging of the support window (u8 frames): box_w x box_h bytes at
   // window offset (box_off, box_off); 0 = direct loads
