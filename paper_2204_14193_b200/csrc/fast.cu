@@ -562,13 +562,6 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       if (!G::PLANAR) {
         const int coloff = (lane - v) & (F - 1);
         const float4 *tp = (const float4 *)region + rowoff * F + coloff;
-#ifdef FSE_TWO_CHAINS
-        // two independent first-max trackers over pairs 0-7 and 8-15 halve
-        // the serial compare/select chain; merged below (the second half
-        // wins only if strictly greater, which keeps row-major-first order)
-        float best2 = -1.f, bx2 = 0.f;
-        int bp2 = 8;
-#endif
 #pragma unroll
         for (int p = 0; p < G::NP; ++p) {
           FSE_CHECK(rowoff + (F == 32 ? 2 * p : p) < G::TROWS);
@@ -583,19 +576,10 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
           const float m = fmaxf(mg.x, mg.y);
 #if FSE_DIAG & 2
           best = fmaxf(best, m);
-#elif defined(FSE_TWO_CHAINS)
-          if (p < 8) {
-            if (m > best) { best = m; bp = p; bx = mg.x; }
-          } else {
-            if (m > best2) { best2 = m; bp2 = p; bx2 = mg.x; }
-          }
 #else
           if (m > best) { best = m; bp = p; bx = mg.x; }
 #endif
         }
-#ifdef FSE_TWO_CHAINS
-        if (best2 > best) { best = best2; bp = bp2; bx = bx2; }
-#endif
       } else {
         const float *Tre = (const float *)region;
         const float *Tim = Tre + G::TROWS * F;
