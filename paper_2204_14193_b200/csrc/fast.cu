@@ -97,6 +97,15 @@ FSE_DEV void ffma2_acc(float2 &acc, float2 a, float b) {
 }
 FSE_DEV float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
+#if FSE_DIAG & 32
+// timing probe (scripts/slot_phase.py): phase timestamps of the current
+// block by slot thread 0, written over the first trace coefficients after
+// the block as T_j - T_0, j = 1..6
+#define FSE_TMARK(j) (tmk[j] = (unsigned)clock())
+#else
+#define FSE_TMARK(j) ((void)0)
+#endif
+
 template <int F> struct SlotPtrs {
   float2 *scratch;  // F x F (non-alias) -- FFT, then trace
   uint4 *xch;       // 2 x NW candidates
@@ -371,6 +380,9 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
 
   const int off = (F - a.B) / 2;
   int loaded = -1;
+#if FSE_DIAG & 32
+  unsigned tmk[7];
+#endif
   for (int round = blockIdx.x; round < a.n_rounds; round += gridDim.x) {
     const int cls = __ldg(a.round_class + round);
     if (cls != loaded) {
@@ -386,6 +398,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       continue;
     }
     if constexpr (TMA) mbar_wait(mbar, *tphase);
+    FSE_TMARK(0);
 
     // ---------------------------------------------------------- load s*w
     FSE_CHECK(b < a.n_blocks && cls < a.n_classes);
@@ -478,6 +491,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         }
       }
       slot_sync<F>(slot);
+      FSE_TMARK(1);
       if constexpr (TMA) {
         if (st == 0) *tphase ^= 1;  // every thread of the slot has waited
         prefetch(round + gridDim.x);  // the staged window has been consumed
@@ -504,6 +518,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         }
       }
       slot_sync<F>(slot);  // the row spectra are consumed; reuse as X
+      FSE_TMARK(2);
 #if FSE_DIAG & 16
       if (false)
 #endif
@@ -518,15 +533,27 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         }
       }
       slot_sync<F>(slot);
-      auto bin = [&](int r, int c) -> float2 {
-        if (c == 0 || c == H) {  // untangle the packed real columns 0 and F/2
-          const float2 yk = S[r * XS], ym = S[((F - r) & (F - 1)) * XS];
-          return c == 0 ? make_float2((yk.x + ym.x) * 0.5f, (yk.y - ym.y) * 0.5f)
-                        : make_float2((yk.y + ym.y) * 0.5f, (ym.x - yk.x) * 0.5f);
+      FSE_TMARK(3);
+      // untangle the packed real columns 0 and F/2 in place (column F/2 of
+      // the scratch is free): thread r <= F/2 owns rows r and -r
+      if (st <= H) {
+        const int r = st, rm = (F - r) & (F - 1);
+        const float2 yk = S[r * XS], ym = S[rm * XS];
+        const float2 x0 = make_float2((yk.x + ym.x) * 0.5f, (yk.y - ym.y) * 0.5f);
+        const float2 xh = make_float2((yk.y + ym.y) * 0.5f, (ym.x - yk.x) * 0.5f);
+        S[r * XS] = x0;
+        S[r * XS + H] = xh;
+        if (rm != r) {
+          S[rm * XS] = make_float2(x0.x, -x0.y);
+          S[rm * XS + H] = make_float2(xh.x, -xh.y);
         }
-        if (c < H) return S[r * XS + c];
-        const float2 z = S[((F - r) & (F - 1)) * XS + (F - c)];
-        return make_float2(z.x, -z.y);
+      }
+      slot_sync<F>(slot);
+      // X[r][c] = S[r][c] for c <= F/2, else conj(S[-r][F - c])
+      auto bin = [&](int r, int c) -> float2 {
+        const bool lo = c <= H;
+        const float2 z = S[lo ? r * XS + c : ((F - r) & (F - 1)) * XS + (F - c)];
+        return make_float2(z.x, lo ? z.y : -z.y);
       };
 #pragma unroll
       for (int p = 0; p < G::NP; ++p) {
@@ -543,6 +570,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     for (int o = 16; o; o >>= 1) e0p += __shfl_xor_sync(0xffffffffu, e0p, o);
     if (lane == 0) sp.red[w] = e0p;
     slot_sync<F>(slot);  // scratch is free from here on (trace area)
+    FSE_TMARK(4);
     float e = 0.f;
     if (st == 0)
       for (int k = 0; k < G::NW; ++k) e += sp.red[k];
@@ -556,6 +584,9 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     const int rowbase = w * G::RPW;
 #pragma unroll 1
     for (int it = 0; it < a.iterations; ++it) {
+#if FSE_DIAG & 32
+      const unsigned clk0 = (unsigned)clock();
+#endif
       const int rowoff = (rowbase - u) & (F - 1);
       float best = -1.f, bx = 0.f;
       int bp = 0;
@@ -641,16 +672,24 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         sp.trace[it] = make_float4(__uint_as_float((unsigned)u | ((unsigned)v << 16)), cre, cim, e);
         if (a.trace_uv) {
           const size_t o = (size_t)b * a.iterations + it;
+#if FSE_DIAG & 32
+          // timing probe: iteration start clock, CTA/slot, iteration duration
+          a.trace_uv[2 * o] = (int)clk0;
+          a.trace_uv[2 * o + 1] = (int)(blockIdx.x * 8 + slot);
+          a.trace_e[o] = (float)((unsigned)clock() - clk0);
+#else
           a.trace_uv[2 * o] = u;
           a.trace_uv[2 * o + 1] = v;
+          a.trace_e[o] = e;
+#endif
           a.trace_c[2 * o] = cre;
           a.trace_c[2 * o + 1] = cim;
-          a.trace_e[o] = e;
         }
       }
       (void)gkey;
     }
     slot_sync<F>(slot);
+    FSE_TMARK(5);
 
     // ------------------------------------------------ synthesis + store
     constexpr int PX = (F / 4) * (F / 4) / G::NT;  // loss pixels per thread
@@ -701,6 +740,12 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       }
     }
     slot_sync<F>(slot);  // trace / scratch reuse by the next block
+#if FSE_DIAG & 32
+    FSE_TMARK(6);
+    if (st == 0 && a.trace_c)
+      for (int j = 1; j < 7 && j < a.iterations; ++j)
+        a.trace_c[2 * ((size_t)b * a.iterations + j)] = (float)(tmk[j] - tmk[0]);
+#endif
   }
 }
 

@@ -14,7 +14,7 @@ for fn in re.split(r"\n\s+Function : ", sass)[1:]:
     if "fast_kernel" not in name:
         continue
     F = re.search(r"ILi(\d+)E", name).group(1) + (" tma" if "ELb1E" in name else "")
-    ins = [l for l in fn.split("\n") if re.search(r"/\*[0-9a-f]{4}\*/", l)]
+    ins = [l for l in fn.split("\n") if re.search(r"/\*[0-9a-f]{4,}\*/", l)]
     best = None
     for l in ins:
         m = re.search(r"BRA(?:\.U)?\s+(?:!?U?P\w+,\s*)?(0x[0-9a-f]+)", l)
@@ -29,3 +29,5 @@ for fn in re.split(r"\n\s+Function : ", sass)[1:]:
                             for l in best)
     print(f"F={F}: loop {len(best)} instrs; MOV={c['MOV'] + c['IMAD']} LDL={c['LDL']} STL={c['STL']} "
           f"FFMA2={c['FFMA2']} LDS={c['LDS']} BRA={c['BRA']}")
+    if os.environ.get("LOOP_DUMP") == F:
+        print("\n".join(best))
