@@ -106,6 +106,28 @@ FSE_DEV float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 #define FSE_TMARK(j) ((void)0)
 #endif
 
+// Exchange-buffer accesses through 32-bit shared-window addresses (the two
+// buffers differ in one address bit, so switching is an XOR).
+FSE_DEV uint4 lds128u(unsigned addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+FSE_DEV void sts128u(unsigned addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// bytes per slot region: [stage] scratch | exchange x 2 | red[16] | mbarrier
+template <int F> constexpr size_t slot_stride(bool tma) {
+  return ((tma ? FG<F>::STAGE : 0) + FG<F>::SCRATCH + 2 * FG<F>::NW * sizeof(uint4) + 64 + 16 +
+          511) & ~(size_t)511;
+}
+
 template <int F> struct SlotPtrs {
   float2 *scratch;  // F x F (non-alias) -- FFT, then trace
   uint4 *xch;       // 2 x NW candidates
@@ -330,13 +352,11 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
   char *region = smem;
   float2 *syn_tw = (float2 *)(smem + G::REGION);  // exp(+2 pi i j / F), j < F
   float2 *fft_tw = syn_tw + F;                     // exp(-2 pi i j / F), j < F
-  // slot regions 128-byte aligned for TMA destinations
-  char *slots_base = TMA ? (char *)(((uintptr_t)(fft_tw + F) + 127) & ~(uintptr_t)127)
-                         : (char *)(fft_tw + F);
+  // slot regions 512-byte aligned: TMA destinations (128 B) and the
+  // exchange double buffer (aligned to its size, <= 512 B)
+  char *slots_base = (char *)(((uintptr_t)(fft_tw + F) + 511) & ~(uintptr_t)511);
   constexpr size_t STG = TMA ? G::STAGE : 0;  // the direct-load variant keeps no staging area
-  const size_t slot_bytes =
-      TMA ? (STG + G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64 + 16 + 127) & ~(size_t)127
-          : G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64;
+  constexpr size_t slot_bytes = slot_stride<F>(TMA);
 
   const int tid = threadIdx.x;
   const int slot = tid / G::NT, st = tid - slot * G::NT;
@@ -425,6 +445,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       float2 *S = sp.scratch;
       const int4 rect = __ldg((const int4 *)a.support_rect + cls);  // (r0, c0, r1, c1)
       const int j0 = rect.x >> 1, j1 = (rect.z + 1) >> 1;
+      const bool inside8 = a.dtype == 0 && wt >= 0 && wl >= 0 && wt + F <= a.H && wl + F <= a.W;
       // warp-uniform trip count: every lane of a warp takes part in each
       // group_fft (it synchronises the warp); idle groups transform zeros
 #if FSE_DIAG & 16
@@ -454,6 +475,25 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
                 xo = s * __ldg(wtab + (2 * j + 1) * F + n);
                 e0p += xo * s;
               }
+            }
+            v[k] = make_float2(xe, xo);
+          }
+        } else if (inside8) {
+          // u8 frame, window inside the image: no bounds checks, one base
+          // pointer per row and immediate offsets (w = 0 outside the
+          // support, and a u8 sample is finite, so s * w needs no mask)
+          const uint8_t *p0 = (const uint8_t *)a.frames + fbase + (size_t)y0 * a.pitch + wl + t;
+          const uint8_t *p1 = p0 + a.pitch;
+          const float *w0 = wtab + (2 * j) * F + t, *w1 = w0 + F;
+#pragma unroll
+          for (int k = 0; k < VPT; ++k) {
+            float xe = 0.f, xo = 0.f;
+            if (act) {
+              const float se = (float)__ldg(p0 + Q * k), so = (float)__ldg(p1 + Q * k);
+              xe = se * __ldg(w0 + Q * k);
+              xo = so * __ldg(w1 + Q * k);
+              e0p += xe * se;
+              e0p += xo * so;
             }
             v[k] = make_float2(xe, xo);
           }
@@ -571,27 +611,27 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     if (lane == 0) sp.red[w] = e0p;
     slot_sync<F>(slot);  // scratch is free from here on (trace area)
     FSE_TMARK(4);
-    float e = 0.f;
-    if (st == 0)
-      for (int k = 0; k < G::NW; ++k) e += sp.red[k];
-
 
     // ------------------------------------------------------- iterations
+    // Loop state is kept minimal (the spectrum takes 64 of the 96 registers):
+    // the selection as one row-major index, the exchange buffer as a 32-bit
+    // shared address; slot thread 0 records (index, R_w[u,v]) only -- the
+    // coefficients, energies and trace outputs are derived after the loop.
     const float ginv = a.gamma * __ldg(a.inv_w00 + cls);
-    const float dinv = a.gamma * (2.f - a.gamma) * __ldg(a.inv_w00 + cls);
     float cre = 0.f, cim = 0.f;
-    int u = 0, v = 0, parity = 0;
+    unsigned gidx = 0;
+    unsigned xc = (unsigned)__cvta_generic_to_shared(sp.xch);
     const int rowbase = w * G::RPW;
 #pragma unroll 1
     for (int it = 0; it < a.iterations; ++it) {
 #if FSE_DIAG & 32
       const unsigned clk0 = (unsigned)clock();
 #endif
-      const int rowoff = (rowbase - u) & (F - 1);
+      const int rowoff = (rowbase - (int)(gidx >> G::LOG)) & (F - 1);
       float best = -1.f, bx = 0.f;
       int bp = 0;
       if (!G::PLANAR) {
-        const int coloff = (lane - v) & (F - 1);
+        const int coloff = (lane - (int)(gidx & (F - 1))) & (F - 1);
         const float4 *tp = (const float4 *)region + rowoff * F + coloff;
 #pragma unroll
         for (int p = 0; p < G::NP; ++p) {
@@ -616,7 +656,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         const float *Tim = Tre + G::TROWS * F;
         int co[4];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) co[h] = (lane + 32 * h - v) & (F - 1);
+        for (int h = 0; h < 4; ++h) co[h] = (lane + 32 * h - (int)(gidx & (F - 1))) & (F - 1);
 #pragma unroll
         for (int p = 0; p < G::NP; ++p) {
           const int r = (rowoff + (p >> 1)) * F;
@@ -645,53 +685,74 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
       are = __shfl_sync(0xffffffffu, are, ow);
       aim = __shfl_sync(0xffffffffu, aim, ow);
-      unsigned gidx = widx, gkey = wmax;
+      gidx = widx;
 #if FSE_DIAG & 1
       if (false) {
 #else
       if (G::NW > 1) {
 #endif
-        uint4 *xc = sp.xch + parity * G::NW;
-        if (lane == 0) xc[w] = make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim));
+        if (lane == 0)
+          sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
         slot_sync<F>(slot);
-        const uint4 cnd = lane < G::NW ? xc[lane] : make_uint4(0u, 0xffffffffu, 0u, 0u);
-        gkey = __reduce_max_sync(0xffffffffu, cnd.x);
+        const uint4 cnd = lane < G::NW ? lds128u(xc + 16u * lane) : make_uint4(0u, 0xffffffffu, 0u, 0u);
+        const unsigned gkey = __reduce_max_sync(0xffffffffu, cnd.x);
         gidx = __reduce_min_sync(0xffffffffu, cnd.x == gkey ? cnd.y : 0xffffffffu);
         const int wl = (int)(gidx / (unsigned)(G::RPW * F));
         are = __shfl_sync(0xffffffffu, __uint_as_float(cnd.z), wl);
         aim = __shfl_sync(0xffffffffu, __uint_as_float(cnd.w), wl);
-        parity ^= 1;
+        xc ^= (unsigned)(G::NW * sizeof(uint4));  // the other buffer next time
       }
-      u = (int)(gidx >> G::LOG);
-      v = (int)(gidx & (F - 1));
       cre = ginv * are;
       cim = ginv * aim;
       if (st == 0) {
-        e -= dinv * (are * are + aim * aim);
         FSE_CHECK(a.trace_scratch || it < G::TRACE_CAP);
-        sp.trace[it] = make_float4(__uint_as_float((unsigned)u | ((unsigned)v << 16)), cre, cim, e);
-        if (a.trace_uv) {
-          const size_t o = (size_t)b * a.iterations + it;
 #if FSE_DIAG & 32
-          // timing probe: iteration start clock, CTA/slot, iteration duration
-          a.trace_uv[2 * o] = (int)clk0;
-          a.trace_uv[2 * o + 1] = (int)(blockIdx.x * 8 + slot);
-          a.trace_e[o] = (float)((unsigned)clock() - clk0);
+        sp.trace[it] = make_float4(__uint_as_float(gidx), are, aim, __uint_as_float(clk0));
 #else
-          a.trace_uv[2 * o] = u;
-          a.trace_uv[2 * o + 1] = v;
-          a.trace_e[o] = e;
+        sp.trace[it] = make_float4(__uint_as_float(gidx), are, aim, 0.f);
 #endif
-          a.trace_c[2 * o] = cre;
-          a.trace_c[2 * o + 1] = cim;
-        }
       }
-      (void)gkey;
     }
     slot_sync<F>(slot);
     FSE_TMARK(5);
 
-    // ------------------------------------------------ synthesis + store
+    // ------------------------------------ coefficients, trace, synthesis
+    // trace[it] = (index, R_w[u,v]) -> (u | v << 16, c, |R_w[u,v]|^2)
+    for (int k = st; k < a.iterations; k += G::NT) {
+      const float4 tr = sp.trace[k];
+      const unsigned gi = __float_as_uint(tr.x);
+      sp.trace[k] = make_float4(__uint_as_float((gi >> G::LOG) | ((gi & (F - 1)) << 16)),
+                                ginv * tr.y, ginv * tr.z, tr.y * tr.y + tr.z * tr.z);
+#if FSE_DIAG & 32
+      sp.trace[k].w = tr.w;
+#endif
+    }
+    slot_sync<F>(slot);
+    if (a.trace_uv) {  // trace outputs; energies e_t = e_{t-1} - gamma (2 - gamma) |R_w[u,v]|^2 / W00
+      if (st == 0) {
+        const float dinv = a.gamma * (2.f - a.gamma) * __ldg(a.inv_w00 + cls);
+        float e = 0.f;
+        for (int k = 0; k < G::NW; ++k) e += sp.red[k];
+        for (int it = 0; it < a.iterations; ++it) {
+          const float4 tr = sp.trace[it];
+          const unsigned uv = __float_as_uint(tr.x);
+          const size_t o = (size_t)b * a.iterations + it;
+          e -= dinv * tr.w;
+#if FSE_DIAG & 32
+          // timing probe: iteration start clock, CTA/slot
+          a.trace_uv[2 * o] = (int)__float_as_uint(tr.w);
+          a.trace_uv[2 * o + 1] = (int)(blockIdx.x * 8 + slot);
+          a.trace_e[o] = 0.f;
+#else
+          a.trace_uv[2 * o] = (int)(uv & 0xffffu);
+          a.trace_uv[2 * o + 1] = (int)(uv >> 16);
+          a.trace_e[o] = e;
+#endif
+          a.trace_c[2 * o] = tr.y;
+          a.trace_c[2 * o + 1] = tr.z;
+        }
+      }
+    }
     constexpr int PX = (F / 4) * (F / 4) / G::NT;  // loss pixels per thread
     float g[PX];
     int pm[PX], pn[PX];
@@ -712,19 +773,9 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       const int tu = (int)(uv & 0xffffu), tv = (int)(uv >> 16);
 #pragma unroll
       for (int k = 0; k < PX; ++k) {
-#ifdef FSE_SYN_SFU
-        // exact integer phase, centred to [-F/2, F/2) so the SFU argument
-        // stays in [-pi, pi) where __sincosf is most accurate (~1e-6 abs)
-        const int j = ((tu * pm[k] + tv * pn[k] + F / 2) & (F - 1)) - F / 2;
-        float sn, cs;
-        __sincosf((float)j * (6.283185307179586f / F), &sn, &cs);
-        g[k] = fmaf(tr.y, cs, g[k]);
-        g[k] = fmaf(-tr.z, sn, g[k]);
-#else
         const float2 t = syn_tw[(tu * pm[k] + tv * pn[k]) & (F - 1)];
         g[k] = fmaf(tr.y, t.x, g[k]);
         g[k] = fmaf(-tr.z, t.y, g[k]);
-#endif
       }
     }
 #pragma unroll
@@ -752,9 +803,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
 template <int F> static size_t fast_smem(int iter_cap) {
   typedef FG<F> G;
   (void)iter_cap;
-  size_t slot_bytes =
-      (G::STAGE + G::SCRATCH + 2 * G::NW * sizeof(uint4) + 64 + 16 + 127) & ~(size_t)127;
-  return G::REGION + 2 * (size_t)F * sizeof(float2) + 128 + G::S * slot_bytes;
+  return G::REGION + 2 * (size_t)F * sizeof(float2) + 512 + G::S * slot_stride<F>(true);
 }
 
 bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {

@@ -11,9 +11,9 @@ sass = subprocess.run(["cuobjdump", "-sass", cub], capture_output=True, text=Tru
 addr = lambda l: int(re.search(r"/\*([0-9a-f]{4,})\*/", l).group(1), 16)
 for fn in re.split(r"\n\s+Function : ", sass)[1:]:
     name = fn.split("\n")[0]
-    if "fast_kernel" not in name:
+    if "fast_kernel" not in name and "fast_iterate" not in name:
         continue
-    F = re.search(r"ILi(\d+)E", name).group(1) + (" tma" if "ELb1E" in name else "")
+    F = re.search(r"ILi(\d+)E", name).group(1) + (" tma" if "ELb1E" in name else "") + (" iter" if "iterate" in name else "")
     ins = [l for l in fn.split("\n") if re.search(r"/\*[0-9a-f]{4,}\*/", l)]
     best = None
     for l in ins:

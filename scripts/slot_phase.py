@@ -19,14 +19,12 @@ for _ in range(2):
     tiles, tr = plan.run(frames, trace=True)
 torch.cuda.synchronize()
 uv = tr["uv"].cpu().numpy().astype(np.int64)
-dur = tr["e"].cpu().numpy()
 clk = uv[:, :, 0] & 0xffffffff
 cta = uv[:, 0, 1] // 8
 slot = uv[:, 0, 1] % 8
 it_period = np.diff(clk, axis=1) & 0xffffffff
 out = {"iter_period_median": float(np.median(it_period)), "iter_period_p10": float(np.percentile(it_period, 10)),
-       "iter_period_p90": float(np.percentile(it_period, 90)),
-       "scan_to_exchange_end_median": float(np.median(dur))}
+       "iter_period_p90": float(np.percentile(it_period, 90))}
 # per CTA: blocks in order of start; gaps between consecutive blocks of the same slot
 gaps, phase = [], []
 for c in np.unique(cta)[:40]:
