@@ -357,7 +357,7 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
             B * B == 2 * (F * F / 32) && iterations > 0;
   if (p->fast) CK(p->alloc((char **)&p->table, (size_t)nc * p->cfg.table_bytes));
   if (p->fast && p->cfg.global_trace)
-    CK(p->alloc(&p->trace_scratch, (size_t)p->cfg.grid * p->cfg.slots * iterations));
+    CK(p->alloc(&p->trace_scratch, (size_t)p->cfg.grid * p->cfg.slots * 2 * iterations));
 
   fse::ClassSetupArgs ca{};
   ca.n_classes = nc; ca.F = F; ca.rho = rho; ca.labels = p->labels; ca.W64 = p->W64;

@@ -62,7 +62,9 @@ template <int F> struct FG {
       PLANAR ? (size_t)TROWS * F * 2 * sizeof(float) : (size_t)TROWS * F * sizeof(float4);
   // real half-spectrum FFT scratch: max(F/2 x (F+1), F x (F/2+1)) complex
   static constexpr size_t SCRATCH = (((size_t)F * (F / 2 + 1) * sizeof(float2) + 15) & ~(size_t)15);
-  static constexpr int TRACE_CAP = (int)(SCRATCH / 16);
+  // iterations whose trace (16 B) and synthesis coefficient (8 B) fit the scratch
+  static constexpr int TRACE_CAP = (int)(SCRATCH / 24);
+  static constexpr int B = F / 4;  // loss block edge (the planner's fast-path condition)
   // TMA window bytes (u8 support box: 32x24, 48x48, 64x64 at the configs)
   static constexpr size_t STAGE = F == 32 ? 1024 : F == 64 ? 2560 : 4096;
   // the length-F FFTs of the setup: QT lanes per FFT, VPT values per lane
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
   int *const tphase = (int *)(mbar + 1);                      // its expected phase
   sp.trace = (float4 *)sp.scratch;  // the FFT scratch holds the trace after setup
   if (a.trace_scratch)  // more iterations than the shared trace holds: per-slot global scratch
-    sp.trace = a.trace_scratch + ((size_t)blockIdx.x * G::S + slot) * a.iterations;
+    sp.trace = a.trace_scratch + ((size_t)blockIdx.x * G::S + slot) * 2 * a.iterations;
 
   for (int j = tid; j < F; j += blockDim.x) {
     double s, c;
@@ -717,12 +719,17 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     FSE_TMARK(5);
 
     // ------------------------------------ coefficients, trace, synthesis
-    // trace[it] = (index, R_w[u,v]) -> (u | v << 16, c, |R_w[u,v]|^2)
+    // trace[it] = (index, R_w[u,v]) -> (u | v << 16, c, |R_w[u,v]|^2), and
+    // c2[it] = c e^{2 pi i u (B/2) / F} for the second pixel row (below)
+    float2 *const c2 = (float2 *)(sp.trace + a.iterations);
     for (int k = st; k < a.iterations; k += G::NT) {
       const float4 tr = sp.trace[k];
-      const unsigned gi = __float_as_uint(tr.x);
-      sp.trace[k] = make_float4(__uint_as_float((gi >> G::LOG) | ((gi & (F - 1)) << 16)),
-                                ginv * tr.y, ginv * tr.z, tr.y * tr.y + tr.z * tr.z);
+      const unsigned gi = __float_as_uint(tr.x), tu = gi >> G::LOG;
+      const float cr = ginv * tr.y, ci = ginv * tr.z;
+      sp.trace[k] = make_float4(__uint_as_float(tu | ((gi & (F - 1)) << 16)), cr, ci,
+                                tr.y * tr.y + tr.z * tr.z);
+      const float2 om = syn_tw[(tu * (G::B / 2)) & (F - 1)];
+      c2[k] = make_float2(cr * om.x - ci * om.y, cr * om.y + ci * om.x);
 #if FSE_DIAG & 32
       sp.trace[k].w = tr.w;
 #endif
@@ -753,41 +760,38 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         }
       }
     }
-    constexpr int PX = (F / 4) * (F / 4) / G::NT;  // loss pixels per thread
-    float g[PX];
-    int pm[PX], pn[PX];
-#pragma unroll
-    for (int k = 0; k < PX; ++k) {
-      const int q = st + k * G::NT;
-      pm[k] = off + q / a.B;
-      pn[k] = off + q % a.B;
-      g[k] = 0.f;
-    }
+    // Synthesis.  Thread st owns loss pixels (m, n) and (m + B/2, n); their
+    // phases differ by u (B/2) / F turns, so one twiddle lookup serves both:
+    //   g(m, n)       += Re{c  t},   t = e^{2 pi i (u m + v n) / F}
+    //   g(m + B/2, n) += Re{c2 t},  c2 = c e^{2 pi i u (B/2) / F}.
+    static_assert(G::B * G::B == 2 * G::NT, "two loss pixels per thread");
+    const int pm = off + st / G::B, pn = off + st % G::B;
+    float g0 = 0.f, g1 = 0.f;
 #if FSE_DIAG & 8
     if (false)
 #endif
-#pragma unroll 2
+#pragma unroll 4
     for (int it = 0; it < a.iterations; ++it) {
       const float4 tr = sp.trace[it];
+      const float2 cc = c2[it];
       const unsigned uv = __float_as_uint(tr.x);
-      const int tu = (int)(uv & 0xffffu), tv = (int)(uv >> 16);
-#pragma unroll
-      for (int k = 0; k < PX; ++k) {
-        const float2 t = syn_tw[(tu * pm[k] + tv * pn[k]) & (F - 1)];
-        g[k] = fmaf(tr.y, t.x, g[k]);
-        g[k] = fmaf(-tr.z, t.y, g[k]);
-      }
+      const float2 t = syn_tw[((int)(uv & 0xffffu) * pm + (int)(uv >> 16) * pn) & (F - 1)];
+      g0 = fmaf(tr.y, t.x, g0);
+      g0 = fmaf(-tr.z, t.y, g0);
+      g1 = fmaf(cc.x, t.x, g1);
+      g1 = fmaf(-cc.y, t.y, g1);
     }
 #pragma unroll
-    for (int k = 0; k < PX; ++k) {
-      const size_t o = (size_t)b * a.B * a.B + (size_t)(pm[k] - off) * a.B + (pn[k] - off);
-      FSE_CHECK(pm[k] - off < a.B && pn[k] - off < a.B && b < a.n_blocks);
+    for (int k = 0; k < 2; ++k) {
+      const float gk = k ? g1 : g0;
+      const size_t o = (size_t)b * (G::B * G::B) + (size_t)(st + k * G::NT);
+      FSE_CHECK(b < a.n_blocks);
       if (a.tile_dtype == 0) {
-        ((uint8_t *)a.tiles)[o] = (uint8_t)__float2int_rn(fminf(fmaxf(g[k], 0.f), 255.f));
+        ((uint8_t *)a.tiles)[o] = (uint8_t)__float2int_rn(fminf(fmaxf(gk, 0.f), 255.f));
       } else if (a.tile_dtype == 1) {
-        ((float *)a.tiles)[o] = g[k];
+        ((float *)a.tiles)[o] = gk;
       } else {
-        ((double *)a.tiles)[o] = (double)g[k];
+        ((double *)a.tiles)[o] = (double)gk;
       }
     }
     slot_sync<F>(slot);  // trace / scratch reuse by the next block
