@@ -62,9 +62,13 @@ template <int F> struct FG {
       PLANAR ? (size_t)TROWS * F * 2 * sizeof(float) : (size_t)TROWS * F * sizeof(float4);
   // real half-spectrum FFT scratch: max(F/2 x (F+1), F x (F/2+1)) complex
   static constexpr size_t SCRATCH = (((size_t)F * (F / 2 + 1) * sizeof(float2) + 15) & ~(size_t)15);
-  // iterations whose trace (16 B) and synthesis coefficient (8 B) fit the scratch
-  static constexpr int TRACE_CAP = (int)(SCRATCH / 24);
   static constexpr int B = F / 4;  // loss block edge (the planner's fast-path condition)
+  // synthesis: SG groups of threads split the coefficients; their partial
+  // pixel sums meet in a reduction buffer at the end of the scratch
+  static constexpr int SG = F == 32 ? 1 : 4;
+  static constexpr size_t SYN_RED = SG > 1 ? (size_t)SG * B * B * sizeof(float) : 0;
+  // iterations whose trace (16 B) and synthesis coefficient (8 B) fit the scratch
+  static constexpr int TRACE_CAP = (int)((SCRATCH - SYN_RED) / 24);
   // TMA window bytes (u8 support box: 32x24, 48x48, 64x64 at the configs)
   static constexpr size_t STAGE = F == 32 ? 1024 : F == 64 ? 2560 : 4096;
   // the length-F FFTs of the setup: QT lanes per FFT, VPT values per lane
@@ -644,10 +648,26 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       if (!G::PLANAR) {
         const int coloff = (lane - (int)(gidx & (F - 1))) & (F - 1);
         const float4 *tp = (const float4 *)region + rowoff * F + coloff;
+#ifndef FSE_PREFETCH
+#define FSE_PREFETCH 2
+#endif
+        // W' loads issued PD pairs ahead of their use (0: left to ptxas).  Without
+        // it ptxas may keep only two load buffers in flight when registers are
+        // tight, exposing the shared-memory latency (measured -10%).
+        constexpr int PD = FSE_PREFETCH;
+        float4 wbuf[PD > 0 ? PD : 1];
+#pragma unroll
+        for (int d = 0; d < PD; ++d) wbuf[d] = tp[(F == 32 ? 2 * d : d) * F];
 #pragma unroll
         for (int p = 0; p < G::NP; ++p) {
           FSE_CHECK(rowoff + (F == 32 ? 2 * p : p) < G::TROWS);
-          const float4 wv = tp[(F == 32 ? 2 * p : p) * F];
+          float4 wv;
+          if constexpr (PD > 0) {
+            wv = wbuf[p % PD];
+            if (p + PD < G::NP) wbuf[p % PD] = tp[(F == 32 ? 2 * (p + PD) : p + PD) * F];
+          } else {
+            wv = tp[(F == 32 ? 2 * p : p) * F];
+          }
           const float2 wr = make_float2(wv.x, wv.y), wi = make_float2(wv.z, wv.w);
           ffma2_acc(Rre[p], wr, -cre);
           ffma2_acc(Rre[p], wi, cim);
@@ -776,38 +796,69 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         }
       }
     }
-    // Synthesis.  Thread st owns loss pixels (m, n) and (m + B/2, n); their
-    // phases differ by u (B/2) / F turns, so one twiddle lookup serves both:
+    // Synthesis.  The slot's threads form SG groups; group sg sums the
+    // coefficients it = sg (mod SG) (short dependent chains), thread gt of a
+    // group owns PP pixel pairs (m, n), (m + B/2, n) with m = m0 + RS k.  The
+    // two pixels of a pair differ in phase by u (B/2) / F = u / 8 turns, so
+    // one twiddle lookup serves both:
     //   g(m, n)       += Re{c  t},   t = e^{2 pi i (u m + v n) / F}
     //   g(m + B/2, n) += Re{c2 t},  c2 = c e^{2 pi i u (B/2) / F}.
-    static_assert(G::B * G::B == 2 * G::NT, "two loss pixels per thread");
-    const int pm = off + st / G::B, pn = off + st % G::B;
-    float g0 = 0.f, g1 = 0.f;
+    constexpr int BB = G::B * G::B, SG = G::SG, GT = G::NT / SG, PP = BB / GT / 2, RS = GT / G::B;
+    static_assert(PP * GT * 2 == BB, "pixel pairs cover the block");
+    const int sg = st / GT, gt = st - sg * GT;
+    const int pm = off + gt / G::B, pn = off + gt % G::B;
+    float g[2 * PP];
+#pragma unroll
+    for (int k = 0; k < 2 * PP; ++k) g[k] = 0.f;
 #if FSE_DIAG & 8
     if (false)
 #endif
-#pragma unroll 4
-    for (int it = 0; it < a.iterations; ++it) {
+#pragma unroll 2
+    for (int it = sg; it < a.iterations; it += SG) {
       const float4 tr = sp.trace[it];
       const float2 cc = c2[it];
       const unsigned uv = __float_as_uint(tr.x);
-      const float2 t = syn_tw[((int)(uv & 0xffffu) * pm + (int)(uv >> 16) * pn) & (F - 1)];
-      g0 = fmaf(tr.y, t.x, g0);
-      g0 = fmaf(-tr.z, t.y, g0);
-      g1 = fmaf(cc.x, t.x, g1);
-      g1 = fmaf(-cc.y, t.y, g1);
-    }
+      const int tu = (int)(uv & 0xffffu), j0 = tu * pm + (int)(uv >> 16) * pn;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const float gk = k ? g1 : g0;
-      const size_t o = (size_t)b * (G::B * G::B) + (size_t)(st + k * G::NT);
-      FSE_CHECK(b < a.n_blocks);
+      for (int k = 0; k < PP; ++k) {
+        const float2 t = syn_tw[(j0 + tu * RS * k) & (F - 1)];
+        g[2 * k] = fmaf(tr.y, t.x, g[2 * k]);
+        g[2 * k] = fmaf(-tr.z, t.y, g[2 * k]);
+        g[2 * k + 1] = fmaf(cc.x, t.x, g[2 * k + 1]);
+        g[2 * k + 1] = fmaf(-cc.y, t.y, g[2 * k + 1]);
+      }
+    }
+    auto store_px = [&](int q, float gk) {
+      const size_t o = (size_t)b * BB + (size_t)q;
+      FSE_CHECK(b < a.n_blocks && q < BB);
       if (a.tile_dtype == 0) {
         ((uint8_t *)a.tiles)[o] = (uint8_t)__float2int_rn(fminf(fmaxf(gk, 0.f), 255.f));
       } else if (a.tile_dtype == 1) {
         ((float *)a.tiles)[o] = gk;
       } else {
         ((double *)a.tiles)[o] = (double)gk;
+      }
+    };
+    if constexpr (SG > 1) {
+      float *red = (float *)((char *)sp.scratch + G::SCRATCH - G::SYN_RED);
+#pragma unroll
+      for (int k = 0; k < PP; ++k) {
+        red[sg * BB + gt + GT * k] = g[2 * k];
+        red[sg * BB + gt + GT * k + BB / 2] = g[2 * k + 1];
+      }
+      slot_sync<F>(slot);
+#pragma unroll
+      for (int q = st; q < BB; q += G::NT) {
+        float s = red[q];
+#pragma unroll
+        for (int s2 = 1; s2 < SG; ++s2) s += red[s2 * BB + q];
+        store_px(q, s);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < PP; ++k) {
+        store_px(gt + GT * k, g[2 * k]);
+        store_px(gt + GT * k + BB / 2, g[2 * k + 1]);
       }
     }
     slot_sync<F>(slot);  // trace / scratch reuse by the next block

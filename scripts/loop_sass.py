@@ -27,7 +27,9 @@ for fn in re.split(r"\n\s+Function : ", sass)[1:]:
         print(f"F={F}: loop not found"); continue
     c = collections.Counter(re.sub(r"^\s*/\*[0-9a-f]+\*/\s*(@!?U?P\w+\s+)?", "", l).split()[0].split(".")[0]
                             for l in best)
+    # distinct LDS.128 destination registers = W' loads the schedule keeps in flight
+    bufs = {m.group(1) for l in best for m in [re.search(r"LDS\.128 (R\d+),", l)] if m}
     print(f"F={F}: loop {len(best)} instrs; MOV={c['MOV'] + c['IMAD']} LDL={c['LDL']} STL={c['STL']} "
-          f"FFMA2={c['FFMA2']} LDS={c['LDS']} BRA={c['BRA']}")
+          f"FFMA2={c['FFMA2']} LDS={c['LDS']} BRA={c['BRA']} ldsbufs={len(bufs)}")
     if os.environ.get("LOOP_DUMP") == F:
         print("\n".join(best))
