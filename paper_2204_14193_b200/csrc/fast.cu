@@ -67,8 +67,8 @@ template <int F> struct FG {
   // pixel sums meet in a reduction buffer at the end of the scratch
   static constexpr int SG = F == 32 ? 1 : 4;
   static constexpr size_t SYN_RED = SG > 1 ? (size_t)SG * B * B * sizeof(float) : 0;
-  // iterations whose trace (16 B) and synthesis coefficient (8 B) fit the scratch
-  static constexpr int TRACE_CAP = (int)((SCRATCH - SYN_RED) / 24);
+  // iterations whose trace (16 B) and synthesis coefficients (16 B) fit the scratch
+  static constexpr int TRACE_CAP = (int)((SCRATCH - SYN_RED) / 32);
   // TMA window bytes (u8 support box: 32x24, 48x48, 64x64 at the configs)
   static constexpr size_t STAGE = F == 32 ? 1024 : F == 64 ? 2560 : 4096;
   // the length-F FFTs of the setup: QT lanes per FFT, VPT values per lane
@@ -756,8 +756,9 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
 
     // ------------------------------------ coefficients, trace, synthesis
     // trace[it] = (index, R_w[u,v]) -> (u | v << 16, c, |R_w[u,v]|^2), and
-    // c2[it] = c e^{2 pi i u (B/2) / F} for the second pixel row (below)
-    float2 *const c2 = (float2 *)(sp.trace + a.iterations);
+    // cq[it] = (c, c2) as (re, re2, -im, -im2) with c2 = c e^{2 pi i u (B/2) / F}
+    // for the second pixel row of the synthesis (below)
+    float4 *const cq = sp.trace + a.iterations;
     for (int k = st; k < a.iterations; k += G::NT) {
       const float4 tr = sp.trace[k];
       const unsigned gi = __float_as_uint(tr.x), tu = gi >> G::LOG;
@@ -765,7 +766,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       sp.trace[k] = make_float4(__uint_as_float(tu | ((gi & (F - 1)) << 16)), cr, ci,
                                 tr.y * tr.y + tr.z * tr.z);
       const float2 om = syn_tw[(tu * (G::B / 2)) & (F - 1)];
-      c2[k] = make_float2(cr * om.x - ci * om.y, cr * om.y + ci * om.x);
+      cq[k] = make_float4(cr, cr * om.x - ci * om.y, -ci, -(cr * om.y + ci * om.x));
 #if FSE_DIAG & 32
       sp.trace[k].w = tr.w;
 #endif
@@ -807,25 +808,23 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     static_assert(PP * GT * 2 == BB, "pixel pairs cover the block");
     const int sg = st / GT, gt = st - sg * GT;
     const int pm = off + gt / G::B, pn = off + gt % G::B;
-    float g[2 * PP];
+    float2 g[PP];  // (pixel (m, n), pixel (m + B/2, n)) of pair k
 #pragma unroll
-    for (int k = 0; k < 2 * PP; ++k) g[k] = 0.f;
+    for (int k = 0; k < PP; ++k) g[k] = make_float2(0.f, 0.f);
 #if FSE_DIAG & 8
     if (false)
 #endif
 #pragma unroll 2
     for (int it = sg; it < a.iterations; it += SG) {
-      const float4 tr = sp.trace[it];
-      const float2 cc = c2[it];
-      const unsigned uv = __float_as_uint(tr.x);
+      const unsigned uv = __float_as_uint(((const float *)sp.trace)[4 * it]);
+      const float4 c4 = cq[it];
+      const float2 cr = make_float2(c4.x, c4.y), ci = make_float2(c4.z, c4.w);
       const int tu = (int)(uv & 0xffffu), j0 = tu * pm + (int)(uv >> 16) * pn;
 #pragma unroll
       for (int k = 0; k < PP; ++k) {
         const float2 t = syn_tw[(j0 + tu * RS * k) & (F - 1)];
-        g[2 * k] = fmaf(tr.y, t.x, g[2 * k]);
-        g[2 * k] = fmaf(-tr.z, t.y, g[2 * k]);
-        g[2 * k + 1] = fmaf(cc.x, t.x, g[2 * k + 1]);
-        g[2 * k + 1] = fmaf(-cc.y, t.y, g[2 * k + 1]);
+        g[k] = ffma2(cr, make_float2(t.x, t.x), g[k]);
+        g[k] = ffma2(ci, make_float2(t.y, t.y), g[k]);
       }
     }
     auto store_px = [&](int q, float gk) {
@@ -843,8 +842,8 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       float *red = (float *)((char *)sp.scratch + G::SCRATCH - G::SYN_RED);
 #pragma unroll
       for (int k = 0; k < PP; ++k) {
-        red[sg * BB + gt + GT * k] = g[2 * k];
-        red[sg * BB + gt + GT * k + BB / 2] = g[2 * k + 1];
+        red[sg * BB + gt + GT * k] = g[k].x;
+        red[sg * BB + gt + GT * k + BB / 2] = g[k].y;
       }
       slot_sync<F>(slot);
 #pragma unroll
@@ -857,8 +856,8 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     } else {
 #pragma unroll
       for (int k = 0; k < PP; ++k) {
-        store_px(gt + GT * k, g[2 * k]);
-        store_px(gt + GT * k + BB / 2, g[2 * k + 1]);
+        store_px(gt + GT * k, g[k].x);
+        store_px(gt + GT * k + BB / 2, g[k].y);
       }
     }
     slot_sync<F>(slot);  // trace / scratch reuse by the next block

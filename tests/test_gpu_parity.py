@@ -308,7 +308,7 @@ def test_rfse_fp32_and_image_plan(fse):
 
 
 def test_fused_trace_beyond_shared_capacity(fse):
-    """I = 1200 > the 533-entry shared trace of F = 64: the trace moves to
+    """I = 1200 > the 400-entry shared trace of F = 64: the trace moves to
     per-slot global scratch (Fig. 3 sweeps run to 2000 basis functions)."""
     from paper_2204_14193_b200.synth import field
     img = field(256, 256, seed=21).astype(np.float32)
