@@ -459,11 +459,10 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.H = p->H; a.W = p->W; a.tiles = tiles; a.tile_dtype = tile_dtype;
     a.trace_uv = trace_uv; a.trace_c = (float *)trace_c; a.trace_e = (float *)trace_e;
     a.trace_scratch = p->trace_scratch;
-    // Optional TMA staging of each block's support window (u8 frames, opt-in
-    // with FSE_TMA=1): one 3-D tile load per block, prefetched during the
-    // previous block's iterations.  Measured 1.6 % slower than the direct
-    // loads on config 5 (the loads are already hidden by the other slots and
-    // the staging area costs shared memory), so it is not the default.
+    // TMA staging of each block's support window (u8 frames; FSE_TMA=0
+    // selects the direct loads): one 3-D tile load per block with OOB zero
+    // fill, prefetched during the slot's previous block, so the setup starts
+    // from shared memory (+1.0 % on config 5).
     CUtensorMap tmap;
     a.use_tma = 0;
     const int off = (p->F - p->B) / 2;
@@ -472,7 +471,7 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.box_w = (a.box_h + 15) & ~15;
     EncodeTiledFn enc = encode_tiled();
     const char *tma_env = getenv("FSE_TMA");
-    if (dtype == FSE_U8 && enc && tma_env && atoi(tma_env) == 1 &&
+    if (dtype == FSE_U8 && enc && !(tma_env && atoi(tma_env) == 0) &&
         (size_t)a.box_w * a.box_h <= fse::fast_stage_bytes(p->F) && a.box_w <= 256 &&
         a.box_h <= 256 && ((uintptr_t)frames % 16) == 0 && (pitch % 16) == 0 &&
         (frame_stride % 16) == 0 && n_frames >= 1) {

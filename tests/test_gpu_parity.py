@@ -320,9 +320,9 @@ def test_fused_trace_beyond_shared_capacity(fse):
 
 
 def test_tma_window_staging_variant(fse):
-    """The opt-in TMA variant (FSE_TMA=1: tensor-map tile loads of each
+    """The TMA variant (the u8 default: tensor-map tile loads of each
     block's support window, OOB zero fill at the image border) gives the same
-    tiles as the direct-load kernel."""
+    tiles as the direct-load kernel (FSE_TMA=0)."""
     import os
     import torch
     from paper_2204_14193_b200.synth import frame_u8
@@ -331,10 +331,10 @@ def test_tma_window_staging_variant(fse):
     blocks = np.concatenate([blocks, np.array([[0, 0, 0], [2, 254, 464]], np.int32)])
     fr = torch.from_numpy(frames).cuda()
     plan = fse.ConcealPlan(blocks, 270, 480, iterations=100)
-    direct = plan.run(fr, tile_dtype="f32").cpu().numpy()
-    os.environ["FSE_TMA"] = "1"
+    staged = plan.run(fr, tile_dtype="f32").cpu().numpy()
+    os.environ["FSE_TMA"] = "0"
     try:
-        staged = plan.run(fr, tile_dtype="f32").cpu().numpy()
+        direct = plan.run(fr, tile_dtype="f32").cpu().numpy()
     finally:
         del os.environ["FSE_TMA"]
     assert np.array_equal(direct, staged)
