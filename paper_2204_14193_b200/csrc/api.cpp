@@ -100,6 +100,7 @@ struct fse_plan {
   double rho = 0, gamma = 0;
   int n_classes = 0, n_rounds = 0;
   bool fast = false;
+  bool tma_aligned = true;  // every window box starts on a 16-byte column (TMA legal)
   fse::FastConfig cfg{};
   // device
   int32_t *blocks = nullptr, *rounds = nullptr, *round_class = nullptr, *block_class = nullptr;
@@ -316,6 +317,8 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
       c = it->second;
     }
     bclass[b] = c;
+    // TMA box start column (left - off + box_off) must be 16-byte aligned
+    if ((left - off + std::max(0, off - border)) % 16 != 0) p->tma_aligned = false;
   }
   const int nc = (int)rects.size();
   p->n_classes = nc;
@@ -459,10 +462,12 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.H = p->H; a.W = p->W; a.tiles = tiles; a.tile_dtype = tile_dtype;
     a.trace_uv = trace_uv; a.trace_c = (float *)trace_c; a.trace_e = (float *)trace_e;
     a.trace_scratch = p->trace_scratch;
-    // TMA staging of each block's support window (u8 frames; FSE_TMA=0
-    // selects the direct loads): one 3-D tile load per block with OOB zero
+    // TMA staging of each block's support window (u8 frames, default for
+    // F=64; FSE_TMA=0/1 forces it off/on): one 3-D tile load per block with OOB zero
     // fill, prefetched during the slot's previous block, so the setup starts
-    // from shared memory (+1.0 % on config 5).
+    // from shared memory (+1.0 % on config 5).  A tile load whose start
+    // column is not 16-byte aligned faults (illegal instruction), so plans
+    // with such boxes (e.g. 8x8 blocks on an 8-pixel grid) load directly.
     CUtensorMap tmap;
     a.use_tma = 0;
     const int off = (p->F - p->B) / 2;
@@ -471,7 +476,9 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.box_w = (a.box_h + 15) & ~15;
     EncodeTiledFn enc = encode_tiled();
     const char *tma_env = getenv("FSE_TMA");
-    if (dtype == FSE_U8 && enc && !(tma_env && atoi(tma_env) == 0) &&
+    const bool tma_default = p->F == 64;  // measured: +1.0 % at F=64, -1.5 % at F=128
+    if (dtype == FSE_U8 && enc && p->tma_aligned &&
+        (tma_env ? atoi(tma_env) == 1 : tma_default) &&
         (size_t)a.box_w * a.box_h <= fse::fast_stage_bytes(p->F) && a.box_w <= 256 &&
         a.box_h <= 256 && ((uintptr_t)frames % 16) == 0 && (pitch % 16) == 0 &&
         (frame_stride % 16) == 0 && n_frames >= 1) {

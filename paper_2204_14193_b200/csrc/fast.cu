@@ -286,18 +286,22 @@ FSE_DEV void dft16(float2 (&x)[16], const float2 *tw, int twstep) {
 template <int F>
 FSE_DEV void group_fft(float2 (&v)[FG<F>::VPT], float2 *ex, int es, const float2 *tw, int t) {
   constexpr int QT = FG<F>::QT;
+  // exchange slot of element (q1, t): XOR-swizzled within each row of QT so
+  // both the writes (fixed q1, lanes t) and the transposed reads (fixed k,
+  // lanes t reading row q1 = t) hit distinct banks
+  auto X = [&](int q1, int tt) -> float2 & { return ex[(q1 * QT + (tt ^ (q1 & (QT - 1)))) * es]; };
   if constexpr (F == 128) {
     dft16(v, tw, F / 16);
 #pragma unroll
     for (int q1 = 1; q1 < 16; ++q1) v[q1] = cmul(v[q1], tw[t * q1]);
 #pragma unroll
-    for (int q1 = 0; q1 < 16; ++q1) ex[(q1 * QT + t) * es] = v[q1];
+    for (int q1 = 0; q1 < 16; ++q1) X(q1, t) = v[q1];
     __syncwarp();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float2 y[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) y[k] = ex[((t + 8 * h) * QT + k) * es];
+      for (int k = 0; k < 8; ++k) y[k] = X(t + 8 * h, k);
       dft8(y);
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[8 * h + k] = y[k];
@@ -307,17 +311,17 @@ FSE_DEV void group_fft(float2 (&v)[FG<F>::VPT], float2 *ex, int es, const float2
 #pragma unroll
     for (int q1 = 1; q1 < 8; ++q1) v[q1] = cmul(v[q1], tw[t * q1]);
 #pragma unroll
-    for (int q1 = 0; q1 < 8; ++q1) ex[(q1 * QT + t) * es] = v[q1];
+    for (int q1 = 0; q1 < 8; ++q1) X(q1, t) = v[q1];
     __syncwarp();
     if (QT == 8) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = ex[(t * QT + k) * es];
+      for (int k = 0; k < 8; ++k) v[k] = X(t, k);
       dft8(v);
     } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        v[k] = ex[(t * QT + k) * es];
-        v[4 + k] = ex[((t + 4) * QT + k) * es];
+        v[k] = X(t, k);
+        v[4 + k] = X(t + 4, k);
       }
       dft4(v[0], v[1], v[2], v[3]);
       dft4(v[4], v[5], v[6], v[7]);
@@ -719,6 +723,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       const unsigned widx = __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
       int pw, mw, ow;
       decode_bin<F>((int)widx, w, pw, mw, ow);
+      FSE_CHECK(pw >= 0 && pw < G::NP && ow >= 0 && ow < 32);
       float are, aim;
       pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
       are = __shfl_sync(0xffffffffu, are, ow);

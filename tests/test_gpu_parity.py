@@ -340,6 +340,29 @@ def test_tma_window_staging_variant(fse):
     assert np.array_equal(direct, staged)
 
 
+@pytest.mark.parametrize("F,B,border", [(32, 8, 8), (64, 16, 16), (128, 32, 16)])
+def test_u8_default_path_matches_direct_loads(fse, F, B, border):
+    """Every window size on u8 frames: the default path, TMA staging forced
+    on (FSE_TMA=1; used only when every box starts 16-byte aligned -- an
+    8-pixel grid of 8x8 blocks is not) and direct loads (FSE_TMA=0) agree."""
+    import os
+    import torch
+    from paper_2204_14193_b200.synth import field_torch
+    frames = field_torch(2, 270, 480, seed=71, device="cuda", edges=True)
+    blocks = fse.frames_pattern(2, 270, 480, B, 0.05, seed=4)
+    plan = fse.ConcealPlan(blocks, 270, 480, fse.Geometry(B, border, F), iterations=60)
+    default = plan.run(frames, tile_dtype="f32").cpu().numpy()
+    try:
+        os.environ["FSE_TMA"] = "0"
+        direct = plan.run(frames, tile_dtype="f32").cpu().numpy()
+        os.environ["FSE_TMA"] = "1"
+        staged = plan.run(frames, tile_dtype="f32").cpu().numpy()
+    finally:
+        del os.environ["FSE_TMA"]
+    assert np.array_equal(default, direct)
+    assert np.array_equal(staged, direct)
+
+
 def test_frame_sharding_is_bitwise_identical(fse):
     """The multi-GPU decomposition (contiguous frame ranges per rank, no
     collective; sharding.py) run rank by rank on one device reproduces the
