@@ -101,6 +101,7 @@ struct fse_plan {
   int n_classes = 0, n_rounds = 0;
   bool fast = false;
   bool tma_aligned = true;  // every window box starts on a 16-byte column (TMA legal)
+  int max_frame = -1;       // largest frame index of the block list
   fse::FastConfig cfg{};
   // device
   int32_t *blocks = nullptr, *rounds = nullptr, *round_class = nullptr, *block_class = nullptr;
@@ -299,6 +300,7 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
   for (int b = 0; b < n_blocks; ++b) {
     const int top = blocks[3 * b + 1], left = blocks[3 * b + 2];
     if (blocks[3 * b] < 0) return fail(FSE_ERR_VALUE, "block %d: negative frame index", b);
+    p->max_frame = std::max(p->max_frame, (int)blocks[3 * b]);
     if (top < 0 || left < 0 || top + B > H || left + B > W)
       return fail(FSE_ERR_CONFIG,
                   "block %d: loss rectangle (%d, %d, %d, %d) extends outside the %dx%d image", b, top,
@@ -444,6 +446,11 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
   if (p->n_blocks == 0) return FSE_OK;
   if (!frames || !tiles) return fail(FSE_ERR_VALUE, "null frames / tiles");
   if (pitch < p->W) return fail(FSE_ERR_VALUE, "pitch %lld < width %d", pitch, p->W);
+  if (p->max_frame >= n_frames)
+    return fail(FSE_ERR_VALUE, "block frame index %d >= n_frames %d", p->max_frame, n_frames);
+  if (n_frames > 1 && frame_stride < (long long)p->H * pitch)
+    return fail(FSE_ERR_VALUE, "frame stride %lld < H x pitch %lld", frame_stride,
+                (long long)p->H * pitch);
   cudaStream_t st = S(stream);
   if (p->iterations == 0) {  // basis_target = 0: transforms only, loss = Re{0} = 0
     size_t bytes = (size_t)p->n_blocks * p->B * p->B * (tile_dtype == 0 ? 1 : tile_dtype == 1 ? 4 : 8);

@@ -127,6 +127,10 @@ def test_errors(fse):
         fse.extrapolate_cfse([[1j] * 64] * 64, mask, cfg)
     with pytest.raises(fse.ConfigError):  # loss block outside the image
         fse.ConcealPlan(np.array([[0, 250, 0]]), 256, 256)
+    import torch
+    plan = fse.ConcealPlan(np.array([[1, 64, 64]], np.int32), 256, 256)
+    with pytest.raises(ValueError):  # block on frame 1 of a one-frame batch
+        plan.run(torch.zeros((1, 256, 256), dtype=torch.uint8, device="cuda"))
 
 
 # ------------------------------------------------------- fused fp32 path
