@@ -74,6 +74,8 @@ template <int F> struct FG {
   // the length-F FFTs of the setup: QT lanes per FFT, VPT values per lane
   static constexpr int QT = F == 128 ? 8 : F / 8;
   static constexpr int VPT = F / QT;
+  // transforms per lane group and pass: every row pair / column in one pass
+  static constexpr int NFT = (F / 2) / (NT / QT);
   static constexpr size_t REGION = TABLE_BYTES;
 };
 
@@ -132,6 +134,15 @@ FSE_DEV void sts128u(unsigned addr, uint4 v) {
 template <int F> constexpr size_t slot_stride(bool tma) {
   return ((tma ? FG<F>::STAGE : 0) + FG<F>::SCRATCH + 2 * FG<F>::NW * sizeof(uint4) + 64 + 16 +
           511) & ~(size_t)511;
+}
+
+// 16-byte shared load at a 32-bit shared-window address (hot loop only)
+FSE_DEV float4 lds128f(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
 }
 
 template <int F> struct SlotPtrs {
@@ -283,56 +294,65 @@ FSE_DEV void dft16(float2 (&x)[16], const float2 *tw, int twstep) {
 // 8 values each); F = 128: radix 16 x 8 (8 lanes, 16 values each).  One
 // exchange through `ex` (element (q1, t) at ex[(q1 * QT + t) * es]); on
 // return v[i] holds X[group_out<F>(t, i)].
-template <int F>
-FSE_DEV void group_fft(float2 (&v)[FG<F>::VPT], float2 *ex, int es, const float2 *tw, int t) {
+template <int F, int NF>
+FSE_DEV void group_fft(float2 (&v)[NF][FG<F>::VPT], float2 *const (&ex)[NF], int es, const float2 *tw,
+                       int t) {
   constexpr int QT = FG<F>::QT;
-  // exchange slot of element (q1, t): XOR-swizzled within each row of QT so
-  // both the writes (fixed q1, lanes t) and the transposed reads (fixed k,
-  // lanes t reading row q1 = t) hit distinct banks
-  auto X = [&](int q1, int tt) -> float2 & { return ex[(q1 * QT + (tt ^ (q1 & (QT - 1)))) * es]; };
+  // NF independent transforms per lane group share the two warp syncs (and
+  // their latencies overlap).  Exchange slot of element (q1, t): XOR-swizzled
+  // within each row of QT so both the writes (fixed q1, lanes t) and the
+  // transposed reads (fixed k, lanes t reading row q1 = t) hit distinct banks.
+  auto X = [&](int f, int q1, int tt) -> float2 & {
+    return ex[f][(q1 * QT + (tt ^ (q1 & (QT - 1)))) * es];
+  };
   if constexpr (F == 128) {
-    dft16(v, tw, F / 16);
 #pragma unroll
-    for (int q1 = 1; q1 < 16; ++q1) v[q1] = cmul(v[q1], tw[t * q1]);
+    for (int f = 0; f < NF; ++f) {
+      dft16(v[f], tw, F / 16);
 #pragma unroll
-    for (int q1 = 0; q1 < 16; ++q1) X(q1, t) = v[q1];
-    __syncwarp();
+      for (int q1 = 1; q1 < 16; ++q1) v[f][q1] = cmul(v[f][q1], tw[t * q1]);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float2 y[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) y[k] = X(t + 8 * h, k);
-      dft8(y);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[8 * h + k] = y[k];
+      for (int q1 = 0; q1 < 16; ++q1) X(f, q1, t) = v[f][q1];
     }
-  } else {
-    dft8(v);
-#pragma unroll
-    for (int q1 = 1; q1 < 8; ++q1) v[q1] = cmul(v[q1], tw[t * q1]);
-#pragma unroll
-    for (int q1 = 0; q1 < 8; ++q1) X(q1, t) = v[q1];
     __syncwarp();
-    if (QT == 8) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = X(t, k);
-      dft8(v);
-    } else {
+    for (int f = 0; f < NF; ++f)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[k] = X(t, k);
-        v[4 + k] = X(t + 4, k);
+      for (int h = 0; h < 2; ++h) {
+        float2 y[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) y[k] = X(f, t + 8 * h, k);
+        dft8(y);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[f][8 * h + k] = y[k];
       }
-      dft4(v[0], v[1], v[2], v[3]);
-      dft4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      dft8(v[f]);
+#pragma unroll
+      for (int q1 = 1; q1 < 8; ++q1) v[f][q1] = cmul(v[f][q1], tw[t * q1]);
+#pragma unroll
+      for (int q1 = 0; q1 < 8; ++q1) X(f, q1, t) = v[f][q1];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      if (QT == 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[f][k] = X(f, t, k);
+        dft8(v[f]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          v[f][k] = X(f, t, k);
+          v[f][4 + k] = X(f, t + 4, k);
+        }
+        dft4(v[f][0], v[f][1], v[f][2], v[f][3]);
+        dft4(v[f][4], v[f][5], v[f][6], v[f][7]);
+      }
     }
   }
-  __syncwarp();
-}
-
-// the two warp synchronisations of group_fft, for lanes with no FFT to do
-FSE_DEV void group_fft_idle() {
-  __syncwarp();
   __syncwarp();
 }
 
@@ -456,15 +476,17 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       const int4 rect = __ldg((const int4 *)a.support_rect + cls);  // (r0, c0, r1, c1)
       const int j0 = rect.x >> 1, j1 = (rect.z + 1) >> 1;
       const bool inside8 = a.dtype == 0 && wt >= 0 && wl >= 0 && wt + F <= a.H && wl + F <= a.W;
-      // warp-uniform trip count: every lane of a warp takes part in each
-      // group_fft (it synchronises the warp); idle groups transform zeros
-#if FSE_DIAG & 16
-      if (false)
-#endif
-      for (int jb = j0; jb < j1; jb += NG) {
-        const int j = jb + g;
-        const bool act = j < j1;
-        float2 v[VPT];
+      // Group g transforms row pairs j = g + NG f (f < NFT): every row pair in
+      // one pass; pairs outside the support rows [j0, j1) transform zeros.
+      constexpr int NFT = G::NFT;
+      static_assert(NFT * NG == H, "row pairs per pass");
+      float2 v[NFT][VPT];
+      float2 *rows[NFT];
+#pragma unroll
+      for (int fi = 0; fi < NFT; ++fi) {
+        const int j = g + NG * fi;
+        rows[fi] = S + j * ZS;
+        const bool act = j >= j0 && j < j1;
         const int y0 = wt + 2 * j;
         if constexpr (TMA) {
           // support window staged by TMA (zeros outside the image)
@@ -486,7 +508,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
                 e0p += xo * s;
               }
             }
-            v[k] = make_float2(xe, xo);
+            v[fi][k] = make_float2(xe, xo);
           }
         } else if (inside8) {
           // u8 frame, window inside the image: no bounds checks, one base
@@ -505,7 +527,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
               e0p += xe * se;
               e0p += xo * so;
             }
-            v[k] = make_float2(xe, xo);
+            v[fi][k] = make_float2(xe, xo);
           }
         } else {
 #pragma unroll
@@ -525,20 +547,22 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
                 e0p += xo * s;
               }
             }
-            v[k] = make_float2(xe, xo);
+            v[fi][k] = make_float2(xe, xo);
           }
         }
-        float2 *row = S + j * ZS;
-        if (act) {
-          group_fft<F>(v, row, 1, fft_tw, t);
+      }
+#if FSE_DIAG & 16
+      if (false)
+#endif
+      {
+        group_fft<F, NFT>(v, rows, 1, fft_tw, t);
+#pragma unroll
+        for (int fi = 0; fi < NFT; ++fi)
 #pragma unroll
           for (int i = 0; i < VPT; ++i) {
-            FSE_CHECK(j * ZS + group_out<F>(t, i) < (int)(G::SCRATCH / sizeof(float2)));
-            row[group_out<F>(t, i)] = v[i];
+            FSE_CHECK((g + NG * fi) * ZS + group_out<F>(t, i) < (int)(G::SCRATCH / sizeof(float2)));
+            rows[fi][group_out<F>(t, i)] = v[fi][i];
           }
-        } else {
-          group_fft_idle();
-        }
       }
       slot_sync<F>(slot);
       FSE_TMARK(1);
@@ -572,14 +596,19 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
 #if FSE_DIAG & 16
       if (false)
 #endif
+      {
+        float2 *cols[CP];
 #pragma unroll
-      for (int pass = 0; pass < CP; ++pass) {
-        const int c = g + pass * NG;
-        group_fft<F>(cin[pass], S + c, XS, fft_tw, t);
+        for (int pass = 0; pass < CP; ++pass) cols[pass] = S + g + pass * NG;
+        group_fft<F, CP>(cin, cols, XS, fft_tw, t);
 #pragma unroll
-        for (int i = 0; i < VPT; ++i) {
-          FSE_CHECK(group_out<F>(t, i) * XS + c < (int)(G::SCRATCH / sizeof(float2)));
-          S[group_out<F>(t, i) * XS + c] = cin[pass][i];
+        for (int pass = 0; pass < CP; ++pass) {
+          const int c = g + pass * NG;
+#pragma unroll
+          for (int i = 0; i < VPT; ++i) {
+            FSE_CHECK(group_out<F>(t, i) * XS + c < (int)(G::SCRATCH / sizeof(float2)));
+            S[group_out<F>(t, i) * XS + c] = cin[pass][i];
+          }
         }
       }
       slot_sync<F>(slot);
@@ -632,6 +661,14 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     unsigned gidx = 0;
     unsigned xc = (unsigned)__cvta_generic_to_shared(sp.xch);
     const int rowbase = w * G::RPW;
+    // Loop-invariant address terms, passed through an identity shuffle so
+    // ptxas keeps them in registers instead of re-deriving them from the
+    // thread/CTA ids (S2R/S2UR) at the latency-critical start of every
+    // iteration: kpos = (first row of the warp) * F | lane, and the table's
+    // 32-bit shared-window address.
+    const unsigned kpos = __shfl_sync(0xffffffffu, (unsigned)(rowbase * F) | (unsigned)lane, lane);
+    const unsigned tbase =
+        __shfl_sync(0xffffffffu, (unsigned)__cvta_generic_to_shared(region), lane);
 #pragma unroll 1
     for (int it = 0; it < a.iterations; ++it) {
 #if FSE_DIAG & 32
@@ -650,8 +687,10 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
 #pragma unroll
       for (int c = 0; c < CH; ++c) { bst[c] = -1.f; bxs[c] = 0.f; bps[c] = c * (G::NP / CH); }
       if (!G::PLANAR) {
-        const int coloff = (lane - (int)(gidx & (F - 1))) & (F - 1);
-        const float4 *tp = (const float4 *)region + rowoff * F + coloff;
+        // table index (rowoff, coloff) = ((rowbase - u) mod F, (lane - v) mod F)
+        constexpr unsigned RM = (unsigned)(F - 1) << G::LOG;
+        const unsigned tp =
+            tbase + ((((kpos - (gidx & RM)) & RM) | ((kpos - gidx) & (unsigned)(F - 1))) << 4);
 #ifndef FSE_PREFETCH
 #define FSE_PREFETCH 2
 #endif
@@ -661,16 +700,17 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         constexpr int PD = FSE_PREFETCH;
         float4 wbuf[PD > 0 ? PD : 1];
 #pragma unroll
-        for (int d = 0; d < PD; ++d) wbuf[d] = tp[(F == 32 ? 2 * d : d) * F];
+        for (int d = 0; d < PD; ++d) wbuf[d] = lds128f(tp + (unsigned)((F == 32 ? 2 * d : d) * F * 16));
 #pragma unroll
         for (int p = 0; p < G::NP; ++p) {
           FSE_CHECK(rowoff + (F == 32 ? 2 * p : p) < G::TROWS);
           float4 wv;
           if constexpr (PD > 0) {
             wv = wbuf[p % PD];
-            if (p + PD < G::NP) wbuf[p % PD] = tp[(F == 32 ? 2 * (p + PD) : p + PD) * F];
+            if (p + PD < G::NP)
+              wbuf[p % PD] = lds128f(tp + (unsigned)((F == 32 ? 2 * (p + PD) : p + PD) * F * 16));
           } else {
-            wv = tp[(F == 32 ? 2 * p : p) * F];
+            wv = lds128f(tp + (unsigned)((F == 32 ? 2 * p : p) * F * 16));
           }
           const float2 wr = make_float2(wv.x, wv.y), wi = make_float2(wv.z, wv.w);
           ffma2_acc(Rre[p], wr, -cre);
@@ -871,6 +911,8 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     if (st == 0 && a.trace_c)
       for (int j = 1; j < 7 && j < a.iterations; ++j)
         a.trace_c[2 * ((size_t)b * a.iterations + j)] = (float)(tmk[j] - tmk[0]);
+    if (st == 0 && !a.trace_c && a.tile_dtype == 1)  // no trace: marks over the f32 tile
+      for (int j = 1; j < 7; ++j) ((float *)a.tiles)[(size_t)b * G::B * G::B + j] = (float)(tmk[j] - tmk[0]);
 #endif
   }
 }

@@ -57,3 +57,15 @@ for j, n in enumerate(names):
     marks[n] = float(np.median(c[:, j] - prev))
     prev = c[:, j]
 print(json.dumps({"phase_cycles_median": marks}))
+
+# the same marks without trace output (tile-based: f32 tiles carry T_j - T_0)
+t2 = plan.run(frames, tile_dtype="f32")
+t2 = plan.run(frames, tile_dtype="f32")
+torch.cuda.synchronize()
+c = t2.reshape(t2.shape[0], -1)[:, 1:7].cpu().numpy()
+prev = np.zeros(len(c))
+marks = {}
+for j, n in enumerate(names):
+    marks[n] = float(np.median(c[:, j] - prev))
+    prev = c[:, j]
+print(json.dumps({"phase_cycles_median_no_trace": marks}))
