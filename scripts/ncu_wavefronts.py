@@ -11,11 +11,14 @@ iw, ie, ii = (hdr.index(k) for k in ("L1 Wavefronts Shared", "L1 Wavefronts Shar
 def fl(x):
     try: return float(x)
     except ValueError: return 0.0
-line, agg = None, defaultdict(lambda: [0.0, 0.0, 0.0])
+line, agg, seen = None, defaultdict(lambda: [0.0, 0.0, 0.0]), set()
 for r in rows[3:]:
     if r and r[0] and r[0].isdigit():
         line = int(r[0]); continue
     if not r or r[0]: continue
+    if r[2] in seen:  # inlined code lists a SASS row under several source lines: count once
+        continue
+    seen.add(r[2])
     a = agg[line]; a[0] += fl(r[iw]); a[1] += fl(r[ie]); a[2] += fl(r[ii])
 B = float(sys.argv[2])
 src = open("paper_2204_14193_b200/csrc/fast.cu").read().split("\n")
