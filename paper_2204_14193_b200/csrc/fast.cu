@@ -790,12 +790,24 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
         if (lane == 0)
           sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
         slot_sync<F>(slot);
+        if constexpr (G::NW == 2) {
+          // two warps: compare with the other warp's candidate in registers
+          // (same total order -- larger |R|^2, then smaller index -- in both)
+          const uint4 o = lds128u(xc + 16u * (unsigned)(w ^ 1));
+          const bool take = o.x > wmax || (o.x == wmax && o.y < widx);
+          if (take) {
+            gidx = o.y;
+            are = __uint_as_float(o.z);
+            aim = __uint_as_float(o.w);
+          }
+        } else {
         const uint4 cnd = lane < G::NW ? lds128u(xc + 16u * lane) : make_uint4(0u, 0xffffffffu, 0u, 0u);
         const unsigned gkey = __reduce_max_sync(0xffffffffu, cnd.x);
         gidx = __reduce_min_sync(0xffffffffu, cnd.x == gkey ? cnd.y : 0xffffffffu);
         const int wl = (int)(gidx / (unsigned)(G::RPW * F));
         are = __shfl_sync(0xffffffffu, __uint_as_float(cnd.z), wl);
         aim = __shfl_sync(0xffffffffu, __uint_as_float(cnd.w), wl);
+        }
         xc ^= (unsigned)(G::NW * sizeof(uint4));  // the other buffer next time
       }
       cre = ginv * are;
