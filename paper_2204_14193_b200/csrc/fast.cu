@@ -1,14 +1,15 @@
 // fast.cu -- fused, register-resident fp32 cFSE kernel for F in {32,64,128}.
 //
-// One lost block per "slot" (a group of NT = F*F/32 threads, i.e. 32
-// spectrum bins per thread held in registers); S slots per CTA share one
-// shared-memory copy of their geometry class's weight spectrum W; one CTA
-// per SM, persistent over a list of same-class rounds.
+// One lost block per "slot" (a group of NT = F*F/BPT threads holding BPT
+// spectrum bins each in registers: BPT = 32 at F=32, 64 at F=64/128); S
+// slots per CTA share one shared-memory copy of their geometry class's
+// weight spectrum W; one CTA per SM, persistent over a list of same-class
+// rounds.
 //
 // Per block (all on chip):
-//   load   s*w of the support ring from the frame (u8/f32/f64)   cfse.py:50
-//   FFT    in-place radix-2 2-D FFT in the slot's shared scratch cfse.py:50
-//   R_w -> registers, exactly Hermitian ((X[k] + conj X[-k]) / 2)
+//   load   s*w of the support window (TMA-staged u8 tile or direct loads)  cfse.py:50
+//   FFT    real-input half-spectrum 2-D FFT in the slot's shared scratch   cfse.py:50
+//   R_w -> registers, exactly Hermitian by construction
 //   I x { R_w -= c W[k-u, l-v]  (FFMA2 on SoA bin pairs, W' from a
 //                                row-extended shared table: one LDS.128
 //                                per bin pair, no index wrap arithmetic)
@@ -20,11 +21,11 @@
 //
 // Bin -> thread mapping (slot thread st = 32 w + lane): warp w owns rows
 // [w*RPW, (w+1)*RPW), lane owns columns lane + 32 h (h < CPL = F/32).  The
-// 32 bins of a thread form 16 SoA pairs (a, b), consecutive in the thread's
-// row-major scan order:
-//   F=32 : a = (2p, lane),            b = (2p+1, lane)
-//   F=64 : a = (16w+p, lane),         b = (16w+p, lane+32)
-//   F=128: a = (8w+p/2, lane+64(p&1)), b = a + (0, 32)
+// BPT bins of a thread form BPT/2 SoA pairs (a, b), consecutive in the
+// thread's row-major scan order (RPW = BPT/CPL):
+//   F=32 : a = (2p, lane),                  b = (2p+1, lane)
+//   F=64 : a = (RPW w + p, lane),           b = a + (0, 32)
+//   F=128: a = (RPW w + p/2, lane+64(p&1)), b = a + (0, 32)
 #include <string.h>
 
 #include "common.cuh"
