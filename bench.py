@@ -108,13 +108,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def measured_ceilings():
-    """Shared-memory ceilings measured on this pool's B200s by scripts/smem_peak.cu."""
+def measured_ceilings(threads: int = 384):
+    """Shared-memory ceilings measured on this pool's B200s by scripts/smem_peak.cu,
+    at the kernel's occupancy: 384 threads x 32 bin pairs (F=64 layout) or
+    640 threads x 16 pairs."""
     try:
         rows = [json.loads(l) for l in open(os.path.join(REPO, "profiles", "r01", "smem_peak.jsonl"))]
-        pick = lambda t: max(r["smem_TBps"] for r in rows if r["test"] == t and r.get("threads") == 640)
+        sfx, thr = ("_p32", 384) if threads == 384 else ("", 640)
+        pick = lambda t: max(r["smem_TBps"] for r in rows if r["test"] == t + sfx and r.get("threads") == thr)
         return {"lds128_TBps": pick("lds128"), "loop_mix_TBps": pick("lds128+6ffma2+argmax"),
-                "source": "profiles/r01/smem_peak.jsonl (scripts/smem_peak.cu)"}
+                "threads": thr, "source": "profiles/r01/smem_peak.jsonl (scripts/smem_peak.cu)"}
     except Exception:
         return None
 
@@ -317,7 +320,7 @@ def main():
     peak_fp32 = sms * 128 * 2 * sm_max * 1e6 / 1e12
     clocks = clk.summary()
     traffic = ncu_traffic(f"config{a.config}")
-    ceil = measured_ceilings()
+    ceil = measured_ceilings(int(plan.info.get("threads", 384)))
     line = {
         "metric": "lost_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,

@@ -3,29 +3,30 @@
 //   lds_ffma2   : LDS.128 + the loop's 6 packed FP32 ops per 16 B (no argmax)
 //   lds_full    : + the loop's 5 ALU ops per 16 B (first-max bookkeeping)
 //   ffma2       : packed FP32 FMA throughput
-// One CTA per SM x 640 threads (the kernel's occupancy) and x 512.
+// One CTA per SM x 640 / 512 threads with 16 pairs per thread, and x 384
+// threads with 32 pairs per thread (the F=64 kernel's current occupancy).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o smem_peak smem_peak.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 
 #define ITERS 4096
 
-template <int mode>
-__global__ void __launch_bounds__(640, 1) lds128(float4 *out) {
+template <int mode, int NPR = 16>
+__global__ void __launch_bounds__(NPR == 16 ? 640 : 384, 1) lds128(float4 *out) {
   extern __shared__ float4 sm[];
   const int tid = threadIdx.x;
   for (int i = tid; i < 8192; i += blockDim.x) sm[i] = make_float4(i, i + 1, i + 2, i + 3);
   __syncthreads();
   const int lane = tid & 31, w = tid >> 5;
-  float2 acc[16], acc2[16];
-  for (int p = 0; p < 16; ++p) { acc[p] = make_float2(p, 1); acc2[p] = make_float2(1, p); }
+  float2 acc[NPR], acc2[NPR];
+  for (int p = 0; p < NPR; ++p) { acc[p] = make_float2(p, 1); acc2[p] = make_float2(1, p); }
   float best = -1.f, bx = 0.f;
   int bp = 0;
   const float c0 = 0.001f * tid, c1 = 0.002f;
   for (int it = 0; it < ITERS; ++it) {
     const float4 *base = sm + ((w * 16 + it) & 63) * 64 + ((lane + it) & 63);
 #pragma unroll
-    for (int p = 0; p < 16; ++p) {
+    for (int p = 0; p < NPR; ++p) {
       float4 v;
       if (mode == 3) {  // the same 16 B as two LDS.64 from planar halves
         const float2 *b2 = (const float2 *)sm + 2 * (((w * 16 + it) & 63) * 64 + ((lane + it) & 63));
@@ -33,7 +34,7 @@ __global__ void __launch_bounds__(640, 1) lds128(float4 *out) {
         float2 hi = b2[(p & 7) * 128 + (p >> 3) * 64 + 8192 / 2];
         v = make_float4(lo.x, lo.y, hi.x, hi.y);
       } else {
-        v = base[(p & 7) * 64 + (p >> 3) * 32];
+        v = base[(p & 7) * 64 + ((p >> 3) & 1) * 32 + (p >> 4) * 512];
       }
       if (mode >= 1) {
         float2 wr = make_float2(v.x, v.y), wi = make_float2(v.z, v.w);
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(640, 1) lds128(float4 *out) {
     }
   }
   float s = best + bx + bp;
-  for (int p = 0; p < 16; ++p) s += acc[p].x + acc[p].y + acc2[p].x + acc2[p].y;
+  for (int p = 0; p < NPR; ++p) s += acc[p].x + acc[p].y + acc2[p].x + acc2[p].y;
   if (s == 12345.f) out[tid] = make_float4(s, 0, 0, 0);
 }
 
@@ -122,6 +123,26 @@ int main() {
       double tbs = bytes / (ms * 1e-3) / 1e12;
       printf("{\"test\": \"%s\", \"threads\": %d, \"smem_TBps\": %.3f, \"bytes_per_clk_per_sm\": %.1f}\n",
              names[mode], threads, tbs, tbs * 1e12 / sms / (clk * 1e3));
+    }
+  }
+  {  // 384 threads x 32 pairs (F=64 kernel occupancy): LDS.128 + mix, + argmax
+    void (*k32[3])(float4 *) = {lds128<0, 32>, lds128<1, 32>, lds128<2, 32>};
+    const char *n32[] = {"lds128_p32", "lds128+6ffma2_p32", "lds128+6ffma2+argmax_p32"};
+    for (int mode = 0; mode < 3; ++mode) {
+      cudaFuncSetAttribute(k32[mode], cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+      k32[mode]<<<sms, 384, 131072>>>(out);
+      cudaEventRecord(e0);
+      for (int r = 0; r < 5; ++r) k32[mode]<<<sms, 384, 131072>>>(out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      cudaError_t err = cudaGetLastError();
+      if (err != cudaSuccess) { printf("error %s\n", cudaGetErrorString(err)); return 1; }
+      double bytes = 5.0 * sms * 384 * (double)ITERS * 32 * 16;
+      double tbs = bytes / (ms * 1e-3) / 1e12;
+      printf("{\"test\": \"%s\", \"threads\": 384, \"smem_TBps\": %.3f, \"bytes_per_clk_per_sm\": %.1f}\n",
+             n32[mode], tbs, tbs * 1e12 / sms / (clk * 1e3));
     }
   }
   cudaFuncSetAttribute(ldsw<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
