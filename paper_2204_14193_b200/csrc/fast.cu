@@ -891,11 +891,16 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       const float4 c4 = cq[it];
       const float2 cr = make_float2(c4.x, c4.y), ci = make_float2(c4.z, c4.w);
       const int tu = (int)(uv & 0xffffu), j0 = tu * pm + (int)(uv >> 16) * pn;
+      // twiddles of the thread's rows m0 + RS k by recurrence t_{k+1} = t_k w,
+      // w = e^{2 pi i u RS / F}: two lookups per coefficient instead of PP
+      float2 t = syn_tw[j0 & (F - 1)];
+      const float2 wv = syn_tw[(tu * RS) & (F - 1)];
+      const float2 wa = make_float2(wv.x, wv.y), wb = make_float2(-wv.y, wv.x);
 #pragma unroll
       for (int k = 0; k < PP; ++k) {
-        const float2 t = syn_tw[(j0 + tu * RS * k) & (F - 1)];
         g[k] = ffma2(cr, make_float2(t.x, t.x), g[k]);
         g[k] = ffma2(ci, make_float2(t.y, t.y), g[k]);
+        if (k + 1 < PP) t = ffma2(make_float2(t.y, t.y), wb, fmul2(make_float2(t.x, t.x), wa));
       }
     }
     auto store_px = [&](int q, float gk) {

@@ -21,7 +21,8 @@ for fn in re.split(r"\n\s+Function : ", sass)[1:]:
         if m and int(m.group(1), 16) < addr(l):
             t = int(m.group(1), 16)
             body = [x for x in ins if t <= addr(x) <= addr(l)]
-            if sum("FFMA2" in x for x in body) >= 40 and (best is None or len(body) < len(best)):
+            if (sum("FFMA2" in x for x in body) >= 40 and sum("LDS" in x for x in body) >= 16
+                    and (best is None or len(body) < len(best))):
                 best = body
     if best is None:
         print(f"F={F}: loop not found"); continue
