@@ -61,3 +61,29 @@ def test_fused_path_random_geometry(fse, seed):
     st = fp32_gate(frames.astype(np.float64), blocks, tiles.cpu().numpy(), get, F, B, border, 0.8, 0.5,
                    iters)
     print(seed, F, B, border, H, W, nf, dtype, iters, len(blocks), st)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fp64_plan_random_geometry(fse, seed):
+    """The fp64 image-level path (reference arithmetic, any window size) on
+    random geometry: tiles within 1e-9 of the fp64 oracle."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2204_14193_b200.synth import field
+    rng = np.random.default_rng(2000 + seed)
+    F = int(rng.choice([16, 24, 32, 48, 64]))
+    B = int(rng.choice([4, 8])) if F < 32 else int(rng.choice([8, 16]))
+    if (F - B) % 2:
+        B += 1
+    border = int(rng.integers(2, (F - B) // 2 + 1))
+    H, W = int(rng.integers(B + 2, 2 * F)), int(rng.integers(B + 2, 2 * F))
+    iters = int(rng.choice([1, 13, 80]))
+    n = 6
+    blocks = np.stack([np.zeros(n, np.int64), rng.integers(0, H - B + 1, n),
+                       rng.integers(0, W - B + 1, n)], 1).astype(np.int32)
+    img = field(H, W, seed=seed)
+    plan = fse.ConcealPlan(blocks, H, W, fse.Geometry(B, border, F), rho_hat=0.8, gamma=0.5,
+                           iterations=iters, precision="fp64")
+    tiles = plan.run(torch.from_numpy(img).cuda(), tile_dtype="f64").cpu().numpy()
+    ref = orc.conceal_blocks(img, blocks, B, border, F, 0.8, 0.5, iters)
+    np.testing.assert_allclose(tiles, ref, rtol=0, atol=1e-9)
