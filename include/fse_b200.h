@@ -46,6 +46,10 @@ extern "C" {
 #define FSE_PREC_F64 0
 #define FSE_PREC_F32 1
 
+/* extrapolation variant of an image-level plan */
+#define FSE_ALG_CFSE 0 /* complex-valued FSE, cfse.py */
+#define FSE_ALG_RFSE 1 /* conjugate-pair (real-valued) FSE, rfse.py */
+
 /* per-window status written by fse_extrapolate (device int32) */
 #define FSE_STATUS_OK 0
 #define FSE_STATUS_EMPTY_SUPPORT 1 /* w00 <= 1e-12*M*N, cfse.py:47-48 */
@@ -156,6 +160,17 @@ typedef struct {
 int fse_plan_create(fse_plan **plan, const int32_t *blocks, int n_blocks, int H, int W, int B,
                     int border, int F, double rho, double gamma, int iterations, int precision,
                     void *stream);
+/* As fse_plan_create, with the variant (FSE_ALG_CFSE / FSE_ALG_RFSE) and an
+ * optional basis_target (>= 0; -1 = none): cFSE runs basis_target
+ * iterations, rFSE stops each block once its basis-function tally (2 per
+ * pair pick, 1 per self-conjugate pick) reaches it, with at most
+ * basis_target iterations (types.py:55-60, rfse.py:184-189).  The fused fp32
+ * kernel serves rFSE at F = 64; other sizes and fp64 use the generic kernel.
+ * Errors additionally: FSE_ERR_CONFIG for a support degenerate for pairwise
+ * selection (rfse.py:50-55). */
+int fse_plan_create_ex(fse_plan **plan, const int32_t *blocks, int n_blocks, int H, int W, int B,
+                       int border, int F, double rho, double gamma, int iterations, int precision,
+                       int algorithm, int basis_target, void *stream);
 int fse_plan_get_info(const fse_plan *plan, fse_plan_info *info);
 int fse_plan_destroy(fse_plan *plan);
 

@@ -24,6 +24,7 @@ FSE_ERR_CUDA = -4
 
 FSE_U8, FSE_F32, FSE_F64 = 0, 1, 2
 FSE_PREC_F64, FSE_PREC_F32 = 0, 1
+FSE_ALG_CFSE, FSE_ALG_RFSE = 0, 1
 
 
 class FseUnsupported(FseError, NotImplementedError):
@@ -57,6 +58,7 @@ _SIGS = {
     "fse_select_basis_f64": ([I, I, P, P, P], I),
     "fse_update_residual_f64": ([I, I, P, P, I, I, D, D, P], I),
     "fse_plan_create": ([ctypes.POINTER(P), P, I, I, I, I, I, I, D, D, I, I, P], I),
+    "fse_plan_create_ex": ([ctypes.POINTER(P), P, I, I, I, I, I, I, D, D, I, I, I, I, P], I),
     "fse_plan_get_info": ([P, ctypes.POINTER(PlanInfo)], I),
     "fse_plan_destroy": ([P], I),
     "fse_plan_run": ([P, P, I, LL, LL, I, P, I, P, P, P, P], I),

@@ -97,6 +97,7 @@ EncodeTiledFn encode_tiled() {
 
 struct fse_plan {
   int n_blocks = 0, H = 0, W = 0, B = 0, border = 0, F = 0, iterations = 0, precision = 0;
+  int algorithm = 0, stop_tally = 0;  // rFSE: stop a block at this basis-function tally
   double rho = 0, gamma = 0;
   int n_classes = 0, n_rounds = 0;
   bool fast = false;
@@ -116,6 +117,7 @@ struct fse_plan {
   double *windows = nullptr, *recon = nullptr, *cs = nullptr, *es = nullptr;
   int64_t *us = nullptr, *vs = nullptr;
   int32_t *status = nullptr;
+  int32_t *selfs = nullptr, *counts = nullptr, *tallies = nullptr;  // generic rFSE outputs
   void *gen_ws = nullptr;
   std::vector<void *> owned;
 
@@ -274,7 +276,21 @@ int fse_update_residual_f64(int M, int N, double *R, const double *W, int u, int
 int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, int W, int B,
                     int border, int F, double rho, double gamma, int iterations, int precision,
                     void *stream) {
+  return fse_plan_create_ex(out, blocks, n_blocks, H, W, B, border, F, rho, gamma, iterations,
+                            precision, FSE_ALG_CFSE, -1, stream);
+}
+
+int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int H, int W, int B,
+                       int border, int F, double rho, double gamma, int iterations, int precision,
+                       int algorithm, int basis_target, void *stream) {
   if (!out) return fail(FSE_ERR_VALUE, "null plan pointer");
+  if (algorithm != FSE_ALG_CFSE && algorithm != FSE_ALG_RFSE)
+    return fail(FSE_ERR_CONFIG, "algorithm must be cfse (0) or rfse (1), got %d", algorithm);
+  // basis_target (types.py:55-60, rfse.py:184-189): cFSE runs that many
+  // iterations; rFSE stops once its basis-function tally reaches it
+  if (basis_target >= 0) {
+    if (algorithm == FSE_ALG_CFSE) iterations = basis_target;
+  }
   *out = nullptr;
   if (int r = check_rho_gamma(rho, gamma)) return r;
   if (iterations < 0) return fail(FSE_ERR_CONFIG, "iterations must be >= 0, got %d", iterations);
@@ -290,6 +306,15 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
   std::unique_ptr<fse_plan> p(new fse_plan());
   p->n_blocks = n_blocks; p->H = H; p->W = W; p->B = B; p->border = border; p->F = F;
   p->iterations = iterations; p->precision = precision; p->rho = rho; p->gamma = gamma;
+  p->algorithm = algorithm;
+  if (algorithm == FSE_ALG_RFSE) {
+    if (basis_target >= 0) {
+      p->iterations = iterations = basis_target;
+      p->stop_tally = basis_target;
+    } else {
+      p->stop_tally = 2 * iterations + 1;  // fixed-count mode (unreachable tally)
+    }
+  }
   const int off = (F - B) / 2;
 
   // geometry classes: the clipped support rectangle (build_mask with
@@ -358,8 +383,11 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
   }
   CK(cudaMemcpyAsync(p->labels, labels.data(), labels.size(), cudaMemcpyHostToDevice, st));
 
-  p->fast = precision == FSE_PREC_F32 && fse::fast_config(F, iterations, sm_count(), &p->cfg) &&
+  p->fast = precision == FSE_PREC_F32 &&
+            fse::fast_config(F, iterations, sm_count(), &p->cfg, algorithm) &&
             B * B == 2 * (F * F / 32) && iterations > 0;
+  double *dmin_dev = nullptr;
+  if (p->fast && algorithm == FSE_ALG_RFSE) CK(p->alloc(&dmin_dev, (size_t)std::max(nc, 1)));
   if (p->fast) CK(p->alloc((char **)&p->table, (size_t)nc * p->cfg.table_bytes));
   if (p->fast && p->cfg.global_trace)
     CK(p->alloc(&p->trace_scratch, (size_t)p->cfg.grid * p->cfg.slots * 2 * iterations));
@@ -368,10 +396,18 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
   ca.n_classes = nc; ca.F = F; ca.rho = rho; ca.labels = p->labels; ca.W64 = p->W64;
   ca.w64 = p->w64; ca.wtab = p->wtab; ca.fast_table = p->fast ? p->table : nullptr;
   ca.fast_table_bytes = p->fast ? p->cfg.table_bytes : 0; ca.w00 = p->w00; ca.tmp = p->tmp;
+  ca.rfse = p->fast && algorithm == FSE_ALG_RFSE; ca.dmin = dmin_dev;
   CK(fse::launch_class_setup(ca, st));
-  std::vector<double> w00(nc);
+  std::vector<double> w00(nc), dmin(nc, 1.0);
   if (nc) CK(cudaMemcpyAsync(w00.data(), p->w00, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (nc && dmin_dev)
+    CK(cudaMemcpyAsync(dmin.data(), dmin_dev, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  for (int c = 0; c < nc; ++c)
+    if (dmin[c] <= 1e-9)  // rfse.py:50-55
+      return fail(FSE_ERR_CONFIG,
+                  "support area is degenerate for pairwise selection (conjugate atoms nearly "
+                  "parallel under the weight)");
   std::vector<float> inv(nc);
   for (int c = 0; c < nc; ++c) {
     if (w00[c] <= 1e-12 * (double)F * F)  // cfse.py:47-48
@@ -411,6 +447,11 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
     CK(p->alloc(&p->cs, C * It * 2));
     CK(p->alloc(&p->es, C * It));
     CK(p->alloc(&p->status, C));
+    if (algorithm == FSE_ALG_RFSE) {
+      CK(p->alloc(&p->selfs, C * It));
+      CK(p->alloc(&p->counts, C));
+      CK(p->alloc(&p->tallies, C));
+    }
     size_t ws = fse::generic_workspace_bytes((int)C, F, F, precision);
     if (ws) CK(p->alloc((char **)&p->gen_ws, ws));
   }
@@ -469,6 +510,8 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.H = p->H; a.W = p->W; a.tiles = tiles; a.tile_dtype = tile_dtype;
     a.trace_uv = trace_uv; a.trace_c = (float *)trace_c; a.trace_e = (float *)trace_e;
     a.trace_scratch = p->trace_scratch;
+    a.algorithm = p->algorithm;
+    a.stop_tally = p->stop_tally;
     // TMA staging of each block's support window (u8 frames, default for
     // F=64; FSE_TMA=0/1 forces it off/on): one 3-D tile load per block with OOB zero
     // fill, prefetched during the slot's previous block, so the setup starts
@@ -509,6 +552,8 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
                                   p->blocks + (size_t)3 * c0, n, F, B, p->windows, st));
     fse::GenArgs a{};
     a.count = n; a.M = F; a.N = F; a.iterations = p->iterations; a.precision = p->precision;
+    a.algorithm = p->algorithm; a.stop_tally = p->algorithm ? p->stop_tally : 0;
+    a.selfs = p->selfs; a.counts = p->counts; a.tallies = p->tallies;
     a.rho = p->rho; a.gamma = p->gamma; a.signal = p->windows; a.labels = p->labels;
     a.labels_stride = (long long)F * F; a.label_index = p->block_class + c0;
     a.recon = p->recon; a.model = nullptr; a.us = p->us; a.vs = p->vs; a.cs = p->cs; a.es = p->es;

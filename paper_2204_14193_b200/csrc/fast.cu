@@ -146,6 +146,27 @@ FSE_DEV float4 lds128f(unsigned addr) {
   return v;
 }
 
+// rFSE (conjugate-pair) variant of the fused kernel, F = 64 only: four
+// blocks per CTA (the pair tables take the shared memory of two slots).
+// Per class, after the W' table: RA4[r][c] = (-bre_a, -bre_b, -bim_a, -bim_b)
+// and RA2[r][c] = (alpha_a, alpha_b) for the pair (r, c), (r, c + 32), c < 32,
+// with the pair selection criterion of bin k written as a quadratic form of
+// a = R_w[k]:  crit = alpha |a|^2 - bre (a.re^2 - a.im^2) - bim a.re a.im
+// (rfse.py:86-111; self-conjugate bins get alpha = -bre = 1/(2 W00)).
+constexpr int RF_SLOTS = 4;
+constexpr size_t RF_T2_BYTES = 64 * 32 * (sizeof(float4) + sizeof(float2));
+template <int F, int ALG> struct KS {  // per-algorithm launch shape
+  static constexpr int S = ALG ? RF_SLOTS : FG<F>::S;
+  static constexpr int CTA = FG<F>::NT * S;
+  static constexpr size_t REGION = ALG ? FG<F>::TABLE_BYTES + RF_T2_BYTES : FG<F>::REGION;
+};
+
+FSE_DEV float2 lds64f(unsigned addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+
 template <int F> struct SlotPtrs {
   float2 *scratch;  // F x F (non-alias) -- FFT, then trace
   uint4 *xch;       // 2 x NW candidates
@@ -388,13 +409,15 @@ FSE_DEV void copy_table(void *dst, const void *src, size_t bytes, int tid, int n
 // by a tensor-map load prefetched during the slot's previous block; TMA =
 // false: direct bounds-checked loads.  Separate instantiations keep each
 // variant's registers for its own path.
-template <int F, bool TMA>
-__global__ void __launch_bounds__(FG<F>::CTA, 1)
+template <int F, bool TMA, int ALG>
+__global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     fast_kernel(FastArgs a, int iter_cap, const __grid_constant__ CUtensorMap tmap) {
   typedef FG<F> G;
+  static_assert(ALG == 0 || F == 64, "the fused rFSE kernel is built for F = 64");
+  constexpr int NS = KS<F, ALG>::S;  // blocks (slots) per CTA
   extern __shared__ __align__(16) char smem[];
   char *region = smem;
-  float2 *syn_tw = (float2 *)(smem + G::REGION);  // exp(+2 pi i j / F), j < F
+  float2 *syn_tw = (float2 *)(smem + KS<F, ALG>::REGION);  // exp(+2 pi i j / F), j < F
   float2 *fft_tw = syn_tw + F;                     // exp(-2 pi i j / F), j < F
   // slot regions 512-byte aligned: TMA destinations (128 B) and the
   // exchange double buffer (aligned to its size, <= 512 B)
@@ -414,7 +437,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
   int *const tphase = (int *)(mbar + 1);                      // its expected phase
   sp.trace = (float4 *)sp.scratch;  // the FFT scratch holds the trace after setup
   if (a.trace_scratch)  // more iterations than the shared trace holds: per-slot global scratch
-    sp.trace = a.trace_scratch + ((size_t)blockIdx.x * G::S + slot) * 2 * a.iterations;
+    sp.trace = a.trace_scratch + ((size_t)blockIdx.x * NS + slot) * 2 * a.iterations;
 
   for (int j = tid; j < F; j += blockDim.x) {
     double s, c;
@@ -434,7 +457,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
   auto prefetch = [&](int rnd) {
     if constexpr (!TMA) return;
     if (st != 0 || rnd >= a.n_rounds) return;
-    const int nb = __ldg(a.rounds + (size_t)rnd * G::S + slot);
+    const int nb = __ldg(a.rounds + (size_t)rnd * NS + slot);
     if (nb < 0) return;
     const int o = (F - a.B) / 2 - a.box_off;  // image offset of the box from the block
     tma_window(sb, &tmap, mbar, (unsigned)(a.box_w * a.box_h), __ldg(a.blocks + 3 * nb + 2) - o,
@@ -456,7 +479,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
       __syncthreads();
       loaded = cls;
     }
-    const int b = __ldg(a.rounds + (size_t)round * G::S + slot);
+    const int b = __ldg(a.rounds + (size_t)round * NS + slot);
     if (b < 0) {  // idle this round: keep the slot's prefetch chain going
       if constexpr (TMA) prefetch(round + gridDim.x);
       continue;
@@ -671,6 +694,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     // shared address; slot thread 0 records (index, R_w[u,v]) only -- the
     // coefficients, energies and trace outputs are derived after the loop.
     const float ginv = a.gamma * __ldg(a.inv_w00 + cls);
+    int nit = a.iterations;  // iterations run (rFSE: fewer when the tally target is met)
     float cre = 0.f, cim = 0.f;
     unsigned gidx = 0;
     unsigned xc = (unsigned)__cvta_generic_to_shared(sp.xch);
@@ -683,6 +707,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     const unsigned kpos = __shfl_sync(0xffffffffu, (unsigned)(rowbase * F) | (unsigned)lane, lane);
     const unsigned tbase =
         __shfl_sync(0xffffffffu, (unsigned)__cvta_generic_to_shared(region), lane);
+    if constexpr (ALG == 0) {
 #pragma unroll 1
     for (int it = 0; it < a.iterations; ++it) {
 #if FSE_DIAG & 32
@@ -822,6 +847,125 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
 #endif
       }
     }
+    } else {
+      // ---------------------------------------- rFSE (rfse.py:69-160)
+      // The selection scans the joint projection of every bin onto its
+      // conjugate pair (crit, a quadratic form of R_w[k] with per-bin
+      // coefficients from the shared pair tables); the winner's projection
+      // (p_re, p_im) follows from its residual and W[2u, 2v] with the
+      // reference's divisions; a pair pick updates R_w with both atoms,
+      // R_w -= c W[k - p] + conj(c) W[k + p], a self-conjugate pick with one.
+      const float w00 = 1.f / __ldg(a.inv_w00 + cls);
+      const unsigned rt4 = __shfl_sync(
+          0xffffffffu,
+          (unsigned)__cvta_generic_to_shared(region + G::TABLE_BYTES) + (unsigned)(rowbase * 32 + lane) * 16u,
+          lane);
+      const unsigned rt2 = __shfl_sync(
+          0xffffffffu,
+          (unsigned)__cvta_generic_to_shared(region + G::TABLE_BYTES + 64 * 32 * sizeof(float4)) +
+              (unsigned)(rowbase * 32 + lane) * 8u,
+          lane);
+      unsigned midx = 0;            // bin of the previous pick's second atom
+      float c2re = 0.f, c2im = 0.f;  // its coefficient (conj c, or 0 after a self-conjugate pick)
+      int tally = 0;
+      nit = 0;
+#pragma unroll 1
+      for (int it = 0; it < a.iterations && tally < a.stop_tally; ++it) {
+        constexpr unsigned RM = (unsigned)(F - 1) << G::LOG;
+        const unsigned tp =
+            tbase + ((((kpos - (gidx & RM)) & RM) | ((kpos - gidx) & (unsigned)(F - 1))) << 4);
+        const unsigned tq =
+            tbase + ((((kpos - (midx & RM)) & RM) | ((kpos - midx) & (unsigned)(F - 1))) << 4);
+        float best = -1.f, bx = 0.f;
+        int bp = 0;
+#pragma unroll
+        for (int p = 0; p < G::NP; ++p) {
+          const float4 wv = lds128f(tp + (unsigned)(p * F * 16));
+          const float4 wq = lds128f(tq + (unsigned)(p * F * 16));
+          const float2 wr = make_float2(wv.x, wv.y), wi = make_float2(wv.z, wv.w);
+          const float2 qr = make_float2(wq.x, wq.y), qi = make_float2(wq.z, wq.w);
+          ffma2_acc(Rre[p], wr, -cre);
+          ffma2_acc(Rre[p], wi, cim);
+          ffma2_acc(Rim[p], wi, -cre);
+          ffma2_acc(Rim[p], wr, -cim);
+          ffma2_acc(Rre[p], qr, -c2re);
+          ffma2_acc(Rre[p], qi, c2im);
+          ffma2_acc(Rim[p], qi, -c2re);
+          ffma2_acc(Rim[p], qr, -c2im);
+          const float2 sr = fmul2(Rre[p], Rre[p]);
+          const float2 mg = ffma2(Rim[p], Rim[p], sr);
+          const float2 sq = ffma2(make_float2(-Rim[p].x, -Rim[p].y), Rim[p], sr);
+          const float2 rr = fmul2(Rre[p], Rim[p]);
+          const float4 b4 = lds128f(rt4 + (unsigned)(p * 32 * 16));
+          const float2 al = lds64f(rt2 + (unsigned)(p * 32 * 8));
+          float2 cr2 = fmul2(al, mg);
+          cr2 = ffma2(make_float2(b4.x, b4.y), sq, cr2);
+          cr2 = ffma2(make_float2(b4.z, b4.w), rr, cr2);
+          const float m = fmaxf(cr2.x, cr2.y);
+          if (m > best) { best = m; bp = p; bx = cr2.x; }
+        }
+        const int myidx = bin_index<F>(w, lane, bp, bx >= best ? 0 : 1);
+        const unsigned key = __float_as_uint(fmaxf(best, 0.f));  // monotone as unsigned
+        const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
+        const unsigned widx =
+            __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
+        int pw, mw, ow;
+        decode_bin<F>((int)widx, w, pw, mw, ow);
+        float are, aim;
+        pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
+        are = __shfl_sync(0xffffffffu, are, ow);
+        aim = __shfl_sync(0xffffffffu, aim, ow);
+        gidx = widx;
+        unsigned gkey = wmax;
+        if (lane == 0)
+          sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
+        slot_sync<F>(slot);
+        {
+          const uint4 o = lds128u(xc + 16u * (unsigned)(w ^ 1));
+          if (o.x > wmax || (o.x == wmax && o.y < widx)) {
+            gidx = o.y;
+            gkey = o.x;
+            are = __uint_as_float(o.z);
+            aim = __uint_as_float(o.w);
+          }
+        }
+        xc ^= (unsigned)(G::NW * sizeof(uint4));
+        // joint projection of the chosen bin (rfse.py:93-103)
+        const unsigned u = gidx >> G::LOG, v = gidx & (F - 1);
+        const bool self = ((2 * u) & (F - 1)) == 0 && ((2 * v) & (F - 1)) == 0;
+        float pr, pi;
+        if (self) {
+          pr = are / w00;
+          pi = 0.f;
+        } else {
+          // W[2u, 2v]: member a of the W' table entry (row 2u, column 2v)
+          const float4 e = lds128f(tbase + ((((2 * u) & (F - 1)) * F + ((2 * v) & (F - 1))) << 4));
+          const float nr = w00 * are - (e.x * are + e.z * aim);
+          const float ni = w00 * aim - (e.z * are - e.x * aim);
+          const float d = w00 * w00 - (e.x * e.x + e.z * e.z);
+          pr = nr / d;
+          pi = ni / d;
+        }
+        // the pair is represented by its smaller row-major member (rfse.py:113-121)
+        unsigned mi = (((F - u) & (F - 1)) << G::LOG) | ((F - v) & (F - 1));
+        if (!self && mi < gidx) {
+          const unsigned t = gidx;
+          gidx = mi;
+          mi = t;
+          pi = -pi;
+        }
+        midx = self ? gidx : mi;
+        cre = a.gamma * pr;
+        cim = a.gamma * pi;
+        c2re = self ? 0.f : cre;
+        c2im = self ? 0.f : -cim;
+        tally += self ? 1 : 2;
+        if (st == 0)
+          sp.trace[it] = make_float4(__uint_as_float(gidx | (self ? 0x80000000u : 0u)), cre, cim,
+                                     __uint_as_float(gkey));
+        nit = it + 1;
+      }
+    }
     slot_sync<F>(slot);
     FSE_TMARK(5);
 
@@ -829,15 +973,29 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     // trace[it] = (index, R_w[u,v]) -> (u | v << 16, c, |R_w[u,v]|^2), and
     // cq[it] = (c, c2) as (re, re2, -im, -im2) with c2 = c e^{2 pi i u (B/2) / F}
     // for the second pixel row of the synthesis (below)
+    // (rFSE: trace[it] = (index | self << 31, c, criterion); a pair pick
+    // contributes c phi + conj(c) phi*, i.e. twice Re{c phi} on real pixels)
     float4 *const cq = sp.trace + a.iterations;
-    for (int k = st; k < a.iterations; k += G::NT) {
+    for (int k = st; k < (ALG ? nit : a.iterations); k += G::NT) {
       const float4 tr = sp.trace[k];
-      const unsigned gi = __float_as_uint(tr.x), tu = gi >> G::LOG;
-      const float cr = ginv * tr.y, ci = ginv * tr.z;
-      sp.trace[k] = make_float4(__uint_as_float(tu | ((gi & (F - 1)) << 16)), cr, ci,
-                                tr.y * tr.y + tr.z * tr.z);
+      float cr, ci, aux, fac = 1.f;
+      unsigned gi = __float_as_uint(tr.x);
+      if constexpr (ALG == 0) {
+        cr = ginv * tr.y;
+        ci = ginv * tr.z;
+        aux = tr.y * tr.y + tr.z * tr.z;
+      } else {
+        fac = (gi >> 31) ? 1.f : 2.f;
+        gi &= 0x7fffffffu;
+        cr = tr.y;
+        ci = tr.z;
+        aux = __uint_as_float(__float_as_uint(tr.w));
+      }
+      const unsigned tu = gi >> G::LOG;
+      sp.trace[k] = make_float4(__uint_as_float(tu | ((gi & (F - 1)) << 16)), cr, ci, aux);
       const float2 om = syn_tw[(tu * (G::B / 2)) & (F - 1)];
-      cq[k] = make_float4(cr, cr * om.x - ci * om.y, -ci, -(cr * om.y + ci * om.x));
+      cq[k] = make_float4(fac * cr, fac * (cr * om.x - ci * om.y), -fac * ci,
+                          -fac * (cr * om.y + ci * om.x));
 #if FSE_DIAG & 32
       sp.trace[k].w = tr.w;
 #endif
@@ -845,13 +1003,23 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     slot_sync<F>(slot);
     if (a.trace_uv) {  // trace outputs; energies e_t = e_{t-1} - gamma (2 - gamma) |R_w[u,v]|^2 / W00
       if (st == 0) {
-        const float dinv = a.gamma * (2.f - a.gamma) * __ldg(a.inv_w00 + cls);
+        // cFSE: e -= gamma (2 - gamma) |R_w[u,v]|^2 / W00;  rFSE: e -= gamma (2 - gamma) crit
+        const float dinv = ALG == 0 ? a.gamma * (2.f - a.gamma) * __ldg(a.inv_w00 + cls)
+                                    : a.gamma * (2.f - a.gamma);
         float e = 0.f;
         for (int k = 0; k < G::NW; ++k) e += sp.red[k];
         for (int it = 0; it < a.iterations; ++it) {
+          const size_t o = (size_t)b * a.iterations + it;
+          if (ALG == 1 && it >= nit) {  // rFSE stopped at the tally target: unused entries
+            a.trace_uv[2 * o] = -1;
+            a.trace_uv[2 * o + 1] = -1;
+            a.trace_c[2 * o] = 0.f;
+            a.trace_c[2 * o + 1] = 0.f;
+            a.trace_e[o] = e;
+            continue;
+          }
           const float4 tr = sp.trace[it];
           const unsigned uv = __float_as_uint(tr.x);
-          const size_t o = (size_t)b * a.iterations + it;
           e -= dinv * tr.w;
 #if FSE_DIAG & 32
           // timing probe: iteration start clock, CTA/slot
@@ -886,7 +1054,7 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
     if (false)
 #endif
 #pragma unroll 2
-    for (int it = sg; it < a.iterations; it += SG) {
+    for (int it = sg; it < (ALG ? nit : a.iterations); it += SG) {
       const unsigned uv = __float_as_uint(((const float *)sp.trace)[4 * it]);
       const float4 c4 = cq[it];
       const float2 cr = make_float2(c4.x, c4.y), ci = make_float2(c4.z, c4.w);
@@ -948,15 +1116,27 @@ __global__ void __launch_bounds__(FG<F>::CTA, 1)
   }
 }
 
-template <int F> static size_t fast_smem(int iter_cap) {
-  typedef FG<F> G;
+template <int F, int ALG = 0> static size_t fast_smem(int iter_cap) {
   (void)iter_cap;
-  return G::REGION + 2 * (size_t)F * sizeof(float2) + 512 + G::S * slot_stride<F>(true);
+  return KS<F, ALG>::REGION + 2 * (size_t)F * sizeof(float2) + 512 +
+         KS<F, ALG>::S * slot_stride<F>(true);
 }
 
-bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
+bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algorithm) {
   size_t smem, tb;
   int S;
+  if (algorithm == 1) {  // fused rFSE: F = 64 only
+    if (F != 64) return false;
+    cfg->global_trace = iterations > FG<64>::TRACE_CAP;
+    smem = fast_smem<64, 1>(0);
+    if (smem > 227 * 1024) return false;
+    cfg->slots = RF_SLOTS;
+    cfg->threads = KS<64, 1>::CTA;
+    cfg->smem_bytes = (int)smem;
+    cfg->grid = sm_count;
+    cfg->table_bytes = FG<64>::TABLE_BYTES + RF_T2_BYTES;
+    return true;
+  }
   switch (F) {
     case 32:
       cfg->global_trace = iterations > FG<32>::TRACE_CAP;
@@ -982,9 +1162,9 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg) {
   return true;
 }
 
-template <int F> static cudaError_t launch_fast_t(const FastArgs &a, const FastConfig &cfg,
-                                                 const CUtensorMap *tmap, cudaStream_t s) {
-  auto kern = tmap ? fast_kernel<F, true> : fast_kernel<F, false>;
+template <int F, int ALG> static cudaError_t launch_fast_t(const FastArgs &a, const FastConfig &cfg,
+                                                          const CUtensorMap *tmap, cudaStream_t s) {
+  auto kern = tmap ? fast_kernel<F, true, ALG> : fast_kernel<F, false, ALG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        cfg.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -998,10 +1178,11 @@ template <int F> static cudaError_t launch_fast_t(const FastArgs &a, const FastC
 
 cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap,
                         cudaStream_t s) {
+  if (a.algorithm == 1) return a.F == 64 ? launch_fast_t<64, 1>(a, cfg, tmap, s) : cudaErrorInvalidValue;
   switch (a.F) {
-    case 32: return launch_fast_t<32>(a, cfg, tmap, s);
-    case 64: return launch_fast_t<64>(a, cfg, tmap, s);
-    case 128: return launch_fast_t<128>(a, cfg, tmap, s);
+    case 32: return launch_fast_t<32, 0>(a, cfg, tmap, s);
+    case 64: return launch_fast_t<64, 0>(a, cfg, tmap, s);
+    case 128: return launch_fast_t<128, 0>(a, cfg, tmap, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -1068,6 +1249,47 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       if (F == 32) x1 = W[((r + 1) % F) * F + q];
       else x1 = W[(r % F) * F + (q + 32) % F];
       T4[i] = make_float4((float)x0.x, (float)x1.x, (float)x0.y, (float)x1.y);
+    }
+    if (a.rfse && F == 64) {
+      // rFSE pair tables (rfse.py:40-55): crit = alpha |a|^2 - bre (a.re^2 - a.im^2)
+      // - bim a.re a.im with, for a pair bin, D = W00^2 - |W2|^2, W2 = W[2k, 2l]:
+      // alpha = 2 W00 / D, bre = 2 W2.re / D, bim = 4 W2.im / D; for a
+      // self-conjugate bin alpha = -bre = 1 / (2 W00), bim = 0.  Stored with
+      // bre, bim negated.  Also the minimum of D / W00^2 over pair bins.
+      const double w00 = W[0].x;
+      float4 *A4 = (float4 *)(tab + FG<64>::TABLE_BYTES);
+      float2 *A2 = (float2 *)(tab + FG<64>::TABLE_BYTES + 64 * 32 * sizeof(float4));
+      double dmin = 1e300;
+      for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
+        const int r = i >> 5, c = i & 31;
+        double al[2], br[2], bi[2];
+        for (int h = 0; h < 2; ++h) {
+          const int cc = c + 32 * h, r2 = (2 * r) % 64, c2 = (2 * cc) % 64;
+          if (r2 == 0 && c2 == 0) {
+            al[h] = 0.5 / w00;
+            br[h] = -0.5 / w00;
+            bi[h] = 0.0;
+          } else {
+            const double2 w2 = W[r2 * 64 + c2];
+            const double d = w00 * w00 - (w2.x * w2.x + w2.y * w2.y);
+            dmin = fmin(dmin, d / (w00 * w00));
+            al[h] = 2.0 * w00 / d;
+            br[h] = 2.0 * w2.x / d;
+            bi[h] = 4.0 * w2.y / d;
+          }
+        }
+        A4[i] = make_float4((float)-br[0], (float)-br[1], (float)-bi[0], (float)-bi[1]);
+        A2[i] = make_float2((float)al[0], (float)al[1]);
+      }
+      // block minimum of dmin -> a.dmin[c]
+      __shared__ double red[512];
+      red[threadIdx.x] = dmin;
+      __syncthreads();
+      for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
+        if ((int)threadIdx.x < s2) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + s2]);
+        __syncthreads();
+      }
+      if (threadIdx.x == 0 && a.dmin) a.dmin[c] = red[0];
     }
   }
 }

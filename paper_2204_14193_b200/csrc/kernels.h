@@ -59,6 +59,8 @@ struct ClassSetupArgs {
   size_t fast_table_bytes;
   double *w00;            // n_classes
   double *tmp;            // n_classes x F x F c128 scratch
+  int rfse;               // also build the fused rFSE pair tables (F = 64)
+  double *dmin;           // n_classes: min over pair bins of D / W00^2 (rfse only)
 };
 cudaError_t launch_class_setup(const ClassSetupArgs &a, cudaStream_t s);
 
@@ -88,6 +90,8 @@ struct FastArgs {
   // TMA staging of the support window (u8 frames): box_w x box_h bytes at
   // window offset (box_off, box_off); 0 = direct loads
   int use_tma, box_w, box_h, box_off;
+  int algorithm;   // 0 = cFSE, 1 = rFSE (F = 64)
+  int stop_tally;  // rFSE: stop a block once its basis-function tally reaches this
 };
 struct FastConfig {
   int slots, threads, smem_bytes, grid;
@@ -95,7 +99,7 @@ struct FastConfig {
   bool global_trace;  // iteration trace kept in global scratch (large I)
 };
 // Returns false when F is not supported by the fused kernel.
-bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg);
+bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algorithm = 0);
 cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap,
                         cudaStream_t s);
 // staging capacity (bytes per slot) of the TMA window for window size F

@@ -55,11 +55,14 @@ class ConcealPlan:
     blocks: int array (n, 3) = (frame, top, left) or (n, 2) = (top, left)
     for a single frame.  precision "fp32" uses the fused register-resident
     kernel (F in {32, 64, 128}); "fp64" the reference-exact per-window path.
+    algorithm "rfse" runs the conjugate-pair variant (rfse.py; fused at F=64
+    in fp32, per-window otherwise); basis_target as in FseConfig.
     """
 
     def __init__(self, blocks, H: int, W: int, geometry: Geometry = Geometry(), *,
                  rho_hat: float = 0.8, gamma: float = 0.5, iterations: int = 100,
-                 precision: str = "fp32", stream=None):
+                 precision: str = "fp32", algorithm: str = "cfse", basis_target=None,
+                 stream=None):
         torch = _lib.require_cuda()
         b = np.asarray(blocks, dtype=np.int32)
         if b.ndim != 2 or b.shape[1] not in (2, 3):
@@ -68,15 +71,19 @@ class ConcealPlan:
             b = np.concatenate([np.zeros((b.shape[0], 1), np.int32), b], axis=1)
         self.blocks = np.ascontiguousarray(b)
         self.H, self.W, self.geometry = int(H), int(W), geometry
-        self.iterations = int(iterations)
+        if algorithm not in ("cfse", "rfse"):
+            raise ConfigError(f"algorithm must be 'cfse' or 'rfse', got {algorithm!r}")
+        self.algorithm = algorithm
+        self.iterations = int(basis_target) if basis_target is not None else int(iterations)
         self.precision = precision
         self.device = torch.cuda.current_device()
         prec = _lib.FSE_PREC_F32 if precision == "fp32" else _lib.FSE_PREC_F64
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().fse_plan_create(
+        _lib.check(_lib.lib().fse_plan_create_ex(
             ctypes.byref(h), self.blocks.ctypes.data_as(ctypes.c_void_p), self.blocks.shape[0],
             self.H, self.W, geometry.B, geometry.border, geometry.F, float(rho_hat), float(gamma),
-            self.iterations, prec, _lib.stream_ptr(stream)))
+            int(iterations), prec, _lib.FSE_ALG_RFSE if algorithm == "rfse" else _lib.FSE_ALG_CFSE,
+            -1 if basis_target is None else int(basis_target), _lib.stream_ptr(stream)))
         self._h = h
         info = _lib.PlanInfo()
         _lib.check(_lib.lib().fse_plan_get_info(self._h, ctypes.byref(info)))

@@ -1,0 +1,26 @@
+"""Fused rFSE vs fused cFSE throughput on config-5 frames at equal basis-function
+counts (cFSE: I = BF iterations; rFSE: basis_target = BF)."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2204_14193_b200 as fse
+from paper_2204_14193_b200.synth import field_torch
+nf = 32
+frames = field_torch(nf, 2160, 3840, seed=5, device="cuda", edges=True)
+blocks = fse.frames_pattern(nf, 2160, 3840, 16, 0.05, seed=5)
+for bf in (100, 200):
+    for alg in ("cfse", "rfse"):
+        kw = dict(iterations=bf) if alg == "cfse" else dict(iterations=bf, basis_target=bf)
+        plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(16, 16, 64), rho_hat=0.8, gamma=0.5,
+                               algorithm=alg, **kw)
+        t = plan.run(frames)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            plan.run(frames, t)
+        e1.record(); torch.cuda.synchronize()
+        s = e0.elapsed_time(e1) / 3 / 1e3
+        print(json.dumps({"algorithm": alg, "basis_functions": bf, "blocks": len(blocks),
+                          "blocks_per_s": len(blocks) / s, "us_per_block": s / len(blocks) * 1e6,
+                          "plan": plan.info}))

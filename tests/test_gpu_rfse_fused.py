@@ -1,0 +1,90 @@
+"""Fused fp32 rFSE (F = 64) against the reference-arithmetic fp64 rFSE path.
+
+The fp64 image-level rFSE plan runs the per-window kernel that reproduces
+the reference's `extrapolate_rfse` (golden-pinned in test_gpu_parity); the
+fused kernel must agree with it per block (max |dpx| <= 0.5 gray levels),
+pick the same canonical pairs in the same order, report the same tally
+semantics (basis_target) and the residual-energy identity."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fse(cuda_ok):
+    import paper_2204_14193_b200 as fse
+    return fse
+
+
+def _plans(fse, blocks, H, W, **kw):
+    geo = fse.Geometry(16, 16, 64)
+    fast = fse.ConcealPlan(blocks, H, W, geo, rho_hat=0.8, gamma=0.5, algorithm="rfse",
+                           precision="fp32", **kw)
+    ref = fse.ConcealPlan(blocks, H, W, geo, rho_hat=0.8, gamma=0.5, algorithm="rfse",
+                          precision="fp64", **kw)
+    assert fast.info["fast_path"] == 1 and ref.info["fast_path"] == 0
+    return fast, ref
+
+
+@pytest.mark.parametrize("dtype,iters,bt", [("u8", 50, None), ("f32", 30, None), ("u8", 100, 100),
+                                            ("f64", 100, 37)])
+def test_fused_rfse_matches_fp64(fse, dtype, iters, bt):
+    import torch
+    from paper_2204_14193_b200.synth import field_torch
+    H, W = 270, 480
+    frames = field_torch(2, H, W, seed=17, device="cuda", edges=True)
+    if dtype != "u8":
+        frames = frames.to(torch.float32 if dtype == "f32" else torch.float64)
+    blocks = fse.frames_pattern(2, H, W, 16, 0.08, seed=6)
+    blocks = np.concatenate([blocks, np.array([[0, 0, 0], [0, 0, W - 16], [1, H - 16, 0],
+                                               [1, H - 16, W - 16]], np.int32)])
+    kw = dict(iterations=iters) if bt is None else dict(iterations=iters, basis_target=bt)
+    fast, ref = _plans(fse, blocks, H, W, **kw)
+    t32, tr = fast.run(frames, tile_dtype="f32", trace=True)
+    t64 = ref.run(frames, tile_dtype="f64")
+    dev = (t32.double() - t64).abs().reshape(len(blocks), -1).max(1).values.cpu().numpy()
+    assert dev.max() <= 0.5, (dev.max(), int((dev > 0.5).sum()))
+    uv = tr["uv"].cpu().numpy()
+    e = tr["e"].cpu().numpy()
+    n_it = fast.iterations
+    for k in range(len(blocks)):
+        used = uv[k, :, 0] >= 0
+        u, v = uv[k, used, 0], uv[k, used, 1]
+        # canonical member: never the larger row-major index of a pair
+        mu, mv = (-u) % 64, (-v) % 64
+        assert np.all(u * 64 + v <= mu * 64 + mv)
+        selfc = ((2 * u) % 64 == 0) & ((2 * v) % 64 == 0)
+        tally = int(np.sum(np.where(selfc, 1, 2)))
+        if bt is None:
+            assert used.sum() == n_it
+        else:  # stops at the first iteration whose tally reaches the target
+            assert tally >= bt and tally - (1 if selfc[-1] else 2) < bt
+        # residual energy decreases monotonically (crit >= 0)
+        assert np.all(np.diff(e[k, used]) <= 1e-3 * e[k, 0])
+
+
+def test_fused_rfse_selection_sequence(fse):
+    """The fused kernel's canonical (u, v) sequence equals the reference-
+    arithmetic per-window rFSE's (fse.extrapolate_rfse, fp64) on interior
+    windows of a u8 frame, up to its first near-tie divergence."""
+    import torch
+    from paper_2204_14193_b200.synth import frame_u8
+    from tests._windows import window_of
+    fr = frame_u8(256, 384, seed=3)
+    blocks = np.array([[0, 64 + 32 * i, 64 + 48 * j] for i in range(3) for j in range(4)], np.int32)
+    fast, _ = _plans(fse, blocks, 256, 384, iterations=60)
+    _, tr = fast.run(torch.from_numpy(fr).cuda(), tile_dtype="f32", trace=True)
+    uv = tr["uv"].cpu().numpy()
+    full = 0
+    for k, (f, t, l) in enumerate(blocks):
+        s, lab = window_of(fr.astype(np.float64), t, l, 64, 16, 16)
+        mask = fse.AreaMask(lab)
+        r = fse.extrapolate_rfse(s, mask, fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=60,
+                                                        fft_dims=(64, 64), algorithm="rfse"))
+        ref_uv = np.array([rec.frequency for rec in r.trace])
+        same = np.all(ref_uv == uv[k], axis=1)
+        first_diff = len(same) if same.all() else int(np.argmin(same))
+        assert first_diff >= 20, (k, first_diff)
+        full += first_diff == len(same)
+    assert full >= len(blocks) // 2
