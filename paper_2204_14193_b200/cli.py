@@ -163,6 +163,7 @@ def cmd_bench(a):
     selected-basis-function count, median of repetitions, on one fixed
     synthetic block instance replicated `--blocks` times.  Rows:
       cfse-fused  -- the fused register-resident fp32 kernel (the product path)
+      rfse-fused  -- its conjugate-pair variant (F = 64), basis_target = count
       cfse, rfse  -- the per-window kernels (same structure for both variants,
                      so their ratio is the paper's loop-structure comparison)."""
     import torch
@@ -207,6 +208,11 @@ def cmd_bench(a):
                                precision="fp32")
             if plan.info["fast_path"]:
                 rows.append(["cfse-fused", bf, *timeit(lambda: plan.run(fr, tile_dtype="f32"))])
+            if a.fft == 64:
+                rplan = ConcealPlan(blocks, H, W, geo, rho_hat=a.rho, gamma=a.gamma, iterations=bf,
+                                    basis_target=bf, precision="fp32", algorithm="rfse")
+                if rplan.info["fast_path"]:
+                    rows.append(["rfse-fused", bf, *timeit(lambda: rplan.run(fr, tile_dtype="f32"))])
         cfg = FseConfig(rho_hat=a.rho, gamma=a.gamma, iterations=max(bf, 1), fft_dims=(a.fft, a.fft),
                         basis_target=bf if bf == 0 else None, precision=prec)
         rows.append(["cfse", bf, *timeit(lambda: extrapolate_cfse_batch(wins, labels, cfg))])
