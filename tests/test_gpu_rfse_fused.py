@@ -88,3 +88,45 @@ def test_fused_rfse_selection_sequence(fse):
         assert first_diff >= 20, (k, first_diff)
         full += first_diff == len(same)
     assert full >= len(blocks) // 2
+
+
+def test_rfse_degenerate_support_raises(fse):
+    """A support confined to one row makes every (k, 0) pair's Gram
+    determinant vanish (W[2k, 0] = W[0, 0]): rfse.py:50-55 raises ConfigError."""
+    lab = np.zeros((32, 32), np.int8)
+    lab[10, 4:28] = 1          # support: one row
+    lab[20:24, 12:16] = 2      # loss
+    cfg = fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=10, fft_dims=(32, 32), algorithm="rfse")
+    with pytest.raises(fse.ConfigError):
+        fse.extrapolate_rfse(np.random.default_rng(0).random((32, 32)) * 255, fse.AreaMask(lab), cfg)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fused_rfse_random_geometry(fse, seed):
+    """Random image sizes (clipped windows), positions, frame types and
+    iteration budgets: fused fp32 rFSE within 0.5 gray levels of fp64."""
+    import torch
+    from paper_2204_14193_b200.synth import field
+    rng = np.random.default_rng(3000 + seed)
+    H, W = int(rng.integers(20, 200)), int(rng.integers(20, 200))
+    n = int(rng.integers(6, 20))
+    blocks = np.stack([np.zeros(n, np.int64), rng.integers(0, H - 16 + 1, n),
+                       rng.integers(0, W - 16 + 1, n)], 1).astype(np.int32)
+    img = field(H, W, seed=seed)
+    dtype = rng.choice(["u8", "f32", "f64"])
+    if dtype == "u8":
+        img = np.clip(np.rint(img), 0, 255).astype(np.uint8)
+    elif dtype == "f32":
+        img = img.astype(np.float32)
+    iters = int(rng.choice([1, 9, 40]))
+    bt = None if rng.random() < 0.5 else int(rng.integers(1, 2 * iters + 1))
+    kw = dict(iterations=iters) if bt is None else dict(iterations=iters, basis_target=bt)
+    try:
+        fast, ref = _plans(fse, blocks, H, W, **kw)
+    except fse.ConfigError:
+        pytest.skip("degenerate pair geometry for this random image")
+    fr = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    t32 = fast.run(fr, tile_dtype="f32")
+    t64 = ref.run(fr, tile_dtype="f64")
+    dev = float((t32.double() - t64).abs().max())
+    assert dev <= 0.5, (seed, H, W, dtype, iters, bt, dev)
