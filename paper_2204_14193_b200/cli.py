@@ -77,18 +77,12 @@ def _conceal_once(img, pattern, a, bf):
 
     geo = Geometry(a.block, a.support, a.fft)
     _config(a, bf)  # validates the parameters (ConfigError)
-    if a.algo == "rfse":
-        from .rfse import conceal_frames_rfse
-
-        t = time.perf_counter()
-        tiles = conceal_frames_rfse(img.astype(np.float64), pattern, geo, rho_hat=a.rho,
-                                    gamma=a.gamma, basis_target=bf, precision=a.precision)
-        dt = time.perf_counter() - t
-        return tiles, dt
     tdt = "f64" if a.precision == "fp64" else "f32"
     t = time.perf_counter()
+    # rFSE: stop at `bf` basis functions (2 per pair pick, rfse.py:184-189)
     tiles = conceal_frames(img, pattern, geo, rho_hat=a.rho, gamma=a.gamma, iterations=bf,
-                           precision=a.precision, tile_dtype=tdt)
+                           precision=a.precision, tile_dtype=tdt, algorithm=a.algo,
+                           basis_target=bf if a.algo == "rfse" else None)
     dt = time.perf_counter() - t
     return tiles, dt
 

@@ -149,7 +149,7 @@ class Concealer:
     def __init__(self, blocks, n_frames: int, H: int, W: int, geometry: Geometry = Geometry(), *,
                  rho_hat: float = 0.8, gamma: float = 0.5, iterations: int = 100,
                  precision: str = "fp32", chunk_frames: int = 16, frame_dtype=np.uint8,
-                 tile_dtype: str = "u8"):
+                 tile_dtype: str = "u8", algorithm: str = "cfse", basis_target=None):
         torch = _lib.require_cuda()
         b = np.asarray(blocks, np.int32).reshape(-1, 3)
         order = np.argsort(b[:, 0], kind="stable")
@@ -166,7 +166,8 @@ class Concealer:
             cb = b[lo:hi].copy()
             cb[:, 0] -= f0
             plan = ConcealPlan(cb, H, W, geometry, rho_hat=rho_hat, gamma=gamma,
-                               iterations=iterations, precision=precision) if hi > lo else None
+                               iterations=iterations, precision=precision, algorithm=algorithm,
+                               basis_target=basis_target) if hi > lo else None
             self.chunks.append((f0, f1, int(lo), int(hi), plan))
         tdt = {"u8": torch.uint8, "f32": torch.float32, "f64": torch.float64}[tile_dtype]
         tt = torch.from_numpy(np.zeros((), self.frame_dtype)).dtype
@@ -232,7 +233,8 @@ class Concealer:
 
 
 def conceal_frames(frames, blocks, geometry: Geometry = Geometry(), *, rho_hat=0.8, gamma=0.5,
-                   iterations=100, precision="fp32", tile_dtype="u8"):
+                   iterations=100, precision="fp32", tile_dtype="u8", algorithm="cfse",
+                   basis_target=None):
     """One-shot form: device or host frames, returns tiles (same side)."""
     import torch
 
@@ -240,7 +242,8 @@ def conceal_frames(frames, blocks, geometry: Geometry = Geometry(), *, rho_hat=0
     f = torch.from_numpy(np.ascontiguousarray(frames)).cuda() if on_host else frames
     f3 = f if f.ndim == 3 else f[None]
     plan = ConcealPlan(blocks, f3.shape[1], f3.shape[2], geometry, rho_hat=rho_hat, gamma=gamma,
-                       iterations=iterations, precision=precision)
+                       iterations=iterations, precision=precision, algorithm=algorithm,
+                       basis_target=basis_target)
     tiles = plan.run(f3, tile_dtype=tile_dtype)
     return tiles.cpu().numpy() if on_host else tiles
 
@@ -263,13 +266,16 @@ def conceal(image: np.ndarray, pattern, config, geometry: Geometry = Geometry())
     corners) in `image` (H x W).  Returns (concealed image, tiles): for 8-bit
     images Re{g} is clamped to [0, 255] and rounded; float images get the
     unclamped model.  `config` is an FseConfig (rho_hat, gamma, loop_bound,
-    precision; fft_dims must equal (F, F))."""
+    precision, algorithm -- cfse or rfse; fft_dims must equal (F, F))."""
     if tuple(config.fft_dims) != (geometry.F, geometry.F):
         raise ConfigError(f"fft_dims {config.fft_dims} != window {geometry.F}")
     img = np.asarray(image)
     tdt = "u8" if img.dtype == np.uint8 else ("f64" if config.precision == "fp64" else "f32")
+    rfse = config.algorithm == "rfse"
     tiles = conceal_frames(img, pattern, geometry, rho_hat=config.rho_hat, gamma=config.gamma,
-                           iterations=config.loop_bound, precision=config.precision, tile_dtype=tdt)
+                           iterations=config.iterations if rfse else config.loop_bound,
+                           precision=config.precision, tile_dtype=tdt, algorithm=config.algorithm,
+                           basis_target=config.basis_target if rfse else None)
     return write_tiles(img, pattern, tiles, geometry.B), tiles
 
 
