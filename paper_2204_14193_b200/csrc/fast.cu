@@ -148,11 +148,10 @@ FSE_DEV float4 lds128f(unsigned addr) {
 
 // rFSE (conjugate-pair) variant of the fused kernel, F = 64 only: four
 // blocks per CTA (the pair tables take the shared memory of two slots).
-// Per class, after the W' table: RA4[r][c] = (-bre_a, -bre_b, -bim_a, -bim_b)
-// and RA2[r][c] = (alpha_a, alpha_b) for the pair (r, c), (r, c + 32), c < 32,
-// with the pair selection criterion of bin k written as a quadratic form of
-// a = R_w[k]:  crit = alpha |a|^2 - bre (a.re^2 - a.im^2) - bim a.re a.im
-// (rfse.py:86-111; self-conjugate bins get alpha = -bre = 1/(2 W00)).
+// Per class, after the W' table: RA4[r][c] = (A_a, A_b, C_a, C_b) and
+// RA2[r][c] = (-D_a, -D_b) for the pair (r, c), (r, c + 32), c < 32, with
+// the pair selection criterion of bin k written as a quadratic form of
+// a = R_w[k]:  crit = A a.re^2 + C a.im^2 - D a.re a.im  (rfse.py:86-111).
 constexpr int RF_SLOTS = 4;
 constexpr size_t RF_T2_BYTES = 64 * 32 * (sizeof(float4) + sizeof(float2));
 template <int F, int ALG> struct KS {  // per-algorithm launch shape
@@ -892,15 +891,14 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           ffma2_acc(Rre[p], qi, c2im);
           ffma2_acc(Rim[p], qi, -c2re);
           ffma2_acc(Rim[p], qr, -c2im);
-          const float2 sr = fmul2(Rre[p], Rre[p]);
-          const float2 mg = ffma2(Rim[p], Rim[p], sr);
-          const float2 sq = ffma2(make_float2(-Rim[p].x, -Rim[p].y), Rim[p], sr);
-          const float2 rr = fmul2(Rre[p], Rim[p]);
-          const float4 b4 = lds128f(rt4 + (unsigned)(p * 32 * 16));
-          const float2 al = lds64f(rt2 + (unsigned)(p * 32 * 8));
-          float2 cr2 = fmul2(al, mg);
-          cr2 = ffma2(make_float2(b4.x, b4.y), sq, cr2);
-          cr2 = ffma2(make_float2(b4.z, b4.w), rr, cr2);
+          // crit = A re^2 + C im^2 - D re im = re (A re - D im) + im (C im)
+          const float4 b4 = lds128f(rt4 + (unsigned)(p * 32 * 16));  // (A_a, A_b, C_a, C_b)
+          const float2 dd = lds64f(rt2 + (unsigned)(p * 32 * 8));     // (-D_a, -D_b)
+          float2 t1 = fmul2(make_float2(b4.x, b4.y), Rre[p]);
+          t1 = ffma2(dd, Rim[p], t1);
+          const float2 t2 = fmul2(make_float2(b4.z, b4.w), Rim[p]);
+          float2 cr2 = fmul2(t1, Rre[p]);
+          cr2 = ffma2(t2, Rim[p], cr2);
           const float m = fmaxf(cr2.x, cr2.y);
           if (m > best) { best = m; bp = p; bx = cr2.x; }
         }
@@ -1251,35 +1249,37 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       T4[i] = make_float4((float)x0.x, (float)x1.x, (float)x0.y, (float)x1.y);
     }
     if (a.rfse && F == 64) {
-      // rFSE pair tables (rfse.py:40-55): crit = alpha |a|^2 - bre (a.re^2 - a.im^2)
-      // - bim a.re a.im with, for a pair bin, D = W00^2 - |W2|^2, W2 = W[2k, 2l]:
-      // alpha = 2 W00 / D, bre = 2 W2.re / D, bim = 4 W2.im / D; for a
-      // self-conjugate bin alpha = -bre = 1 / (2 W00), bim = 0.  Stored with
-      // bre, bim negated.  Also the minimum of D / W00^2 over pair bins.
+      // rFSE pair tables (rfse.py:40-55, 86-111): the pair criterion
+      // 2 (p.re a.re + p.im a.im) with p = [[W00 - W2.re, -W2.im], [-W2.im,
+      // W00 + W2.re]] a / Dt, Dt = W00^2 - |W2|^2, W2 = W[2k, 2l], is
+      // crit = A a.re^2 + C a.im^2 - D a.re a.im with A = 2 (W00 - W2.re) / Dt,
+      // C = 2 (W00 + W2.re) / Dt, D = 4 W2.im / Dt; a self-conjugate bin
+      // (crit = a.re^2 / W00) has A = 1 / W00, C = D = 0.  Also the minimum of
+      // Dt / W00^2 over pair bins.
       const double w00 = W[0].x;
       float4 *A4 = (float4 *)(tab + FG<64>::TABLE_BYTES);
       float2 *A2 = (float2 *)(tab + FG<64>::TABLE_BYTES + 64 * 32 * sizeof(float4));
       double dmin = 1e300;
       for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
         const int r = i >> 5, c = i & 31;
-        double al[2], br[2], bi[2];
+        double qa[2], qc[2], qd[2];
         for (int h = 0; h < 2; ++h) {
           const int cc = c + 32 * h, r2 = (2 * r) % 64, c2 = (2 * cc) % 64;
           if (r2 == 0 && c2 == 0) {
-            al[h] = 0.5 / w00;
-            br[h] = -0.5 / w00;
-            bi[h] = 0.0;
+            qa[h] = 1.0 / w00;
+            qc[h] = 0.0;
+            qd[h] = 0.0;
           } else {
             const double2 w2 = W[r2 * 64 + c2];
             const double d = w00 * w00 - (w2.x * w2.x + w2.y * w2.y);
             dmin = fmin(dmin, d / (w00 * w00));
-            al[h] = 2.0 * w00 / d;
-            br[h] = 2.0 * w2.x / d;
-            bi[h] = 4.0 * w2.y / d;
+            qa[h] = 2.0 * (w00 - w2.x) / d;
+            qc[h] = 2.0 * (w00 + w2.x) / d;
+            qd[h] = 4.0 * w2.y / d;
           }
         }
-        A4[i] = make_float4((float)-br[0], (float)-br[1], (float)-bi[0], (float)-bi[1]);
-        A2[i] = make_float2((float)al[0], (float)al[1]);
+        A4[i] = make_float4((float)qa[0], (float)qa[1], (float)qc[0], (float)qc[1]);
+        A2[i] = make_float2((float)-qd[0], (float)-qd[1]);
       }
       // block minimum of dmin -> a.dmin[c]
       __shared__ double red[512];
