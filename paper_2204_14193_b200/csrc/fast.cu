@@ -932,8 +932,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         const unsigned u = gidx >> G::LOG, v = gidx & (F - 1);
         const bool self = ((2 * u) & (F - 1)) == 0 && ((2 * v) & (F - 1)) == 0;
         float pr, pi;
+        // (fast-path divisions: an IEEE '/' calls a slow-path subroutine whose
+        // calling convention makes ptxas move the spectrum registers each iteration)
         if (self) {
-          pr = are / w00;
+          pr = __fdividef(are, w00);
           pi = 0.f;
         } else {
           // W[2u, 2v]: member a of the W' table entry (row 2u, column 2v)
@@ -941,8 +943,9 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           const float nr = w00 * are - (e.x * are + e.z * aim);
           const float ni = w00 * aim - (e.z * are - e.x * aim);
           const float d = w00 * w00 - (e.x * e.x + e.z * e.z);
-          pr = nr / d;
-          pi = ni / d;
+          const float rd = __fdividef(1.f, d);
+          pr = nr * rd;
+          pi = ni * rd;
         }
         // the pair is represented by its smaller row-major member (rfse.py:113-121)
         unsigned mi = (((F - u) & (F - 1)) << G::LOG) | ((F - v) & (F - 1));
