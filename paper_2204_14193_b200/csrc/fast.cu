@@ -115,6 +115,29 @@ FSE_DEV float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 #define FSE_TMARK(j) ((void)0)
 #endif
 
+// three-input maximum (FMNMX3, sm_100)
+FSE_DEV float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+#ifndef FSE_MAX3
+#define FSE_MAX3 0  // FMNMX3 running maximum: one op fewer per pair, measured -3 % (F=64)
+#endif
+// first-max tracker step over bin pair p with |R|^2 = (mg.x, mg.y): the
+// larger value strictly above the running maximum wins, member a on equal
+// values (bxs keeps member a's value to resolve the member afterwards)
+FSE_DEV void first_max(float &bst, int &bps, float &bxs, float2 mg, int p) {
+#if FSE_MAX3
+  const float nb = fmax3(bst, mg.x, mg.y);  // the running maximum is the only dependent op
+  if (nb > bst) { bps = p; bxs = mg.x; }
+  bst = nb;
+#else
+  const float m = fmaxf(mg.x, mg.y);
+  if (m > bst) { bst = m; bps = p; bxs = mg.x; }
+#endif
+}
+
 // Exchange-buffer accesses through 32-bit shared-window addresses (the two
 // buffers differ in one address bit, so switching is an XOR).
 FSE_DEV uint4 lds128u(unsigned addr) {
@@ -719,7 +742,13 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       // CH independent first-max trackers over consecutive pair ranges
       // (shorter dependent compare/select chains), merged in order below;
       // measured best: 1 (2 helped the 32-bins-per-thread F = 64 variant)
-      constexpr int CH = F == 64 ? FSE_CHAINS64 : 1;
+#ifndef FSE_XTREE
+#define FSE_XTREE 1  // F=128: register merge of the 8 warp candidates (+0.6 %)
+#endif
+#ifndef FSE_CHAINS128
+#define FSE_CHAINS128 1
+#endif
+      constexpr int CH = F == 64 ? FSE_CHAINS64 : F == 128 ? FSE_CHAINS128 : 1;
       float bst[CH], bxs[CH];
       int bps[CH];
 #pragma unroll
@@ -757,12 +786,11 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           ffma2_acc(Rim[p], wr, -cim);
           float2 mg = fmul2(Rre[p], Rre[p]);
           mg = ffma2(Rim[p], Rim[p], mg);
-          const float m = fmaxf(mg.x, mg.y);
           const int ch = p / (G::NP / CH);
 #if FSE_DIAG & 2
-          bst[ch] = fmaxf(bst[ch], m);
+          bst[ch] = fmax3(bst[ch], mg.x, mg.y);
 #else
-          if (m > bst[ch]) { bst[ch] = m; bps[ch] = p; bxs[ch] = mg.x; }
+          first_max(bst[ch], bps[ch], bxs[ch], mg, p);
 #endif
         }
       } else {
@@ -784,9 +812,8 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           ffma2_acc(Rim[p], wr, -cim);
           float2 mg = fmul2(Rre[p], Rre[p]);
           mg = ffma2(Rim[p], Rim[p], mg);
-          const float m = fmaxf(mg.x, mg.y);
           const int ch = p / (G::NP / CH);
-          if (m > bst[ch]) { bst[ch] = m; bps[ch] = p; bxs[ch] = mg.x; }
+          first_max(bst[ch], bps[ch], bxs[ch], mg, p);
         }
       }
       float best = bst[0], bx = bxs[0];
@@ -825,6 +852,22 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
             are = __uint_as_float(o.z);
             aim = __uint_as_float(o.w);
           }
+        } else if (FSE_XTREE) {
+          // every lane reads all NW candidates (broadcast loads) and merges
+          // them pairwise in registers; warp w owns rows [w RPW, (w+1) RPW),
+          // so on equal |R|^2 the lower warp holds the smaller index and the
+          // left operand wins ties
+          uint4 cd[G::NW];
+#pragma unroll
+          for (int j = 0; j < G::NW; ++j) cd[j] = lds128u(xc + 16u * (unsigned)j);
+#pragma unroll
+          for (int s = 1; s < G::NW; s *= 2)
+#pragma unroll
+            for (int j = 0; j + s < G::NW; j += 2 * s)
+              if (cd[j + s].x > cd[j].x) cd[j] = cd[j + s];
+          gidx = cd[0].y;
+          are = __uint_as_float(cd[0].z);
+          aim = __uint_as_float(cd[0].w);
         } else {
         const uint4 cnd = lane < G::NW ? lds128u(xc + 16u * lane) : make_uint4(0u, 0xffffffffu, 0u, 0u);
         const unsigned gkey = __reduce_max_sync(0xffffffffu, cnd.x);

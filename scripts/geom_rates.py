@@ -8,7 +8,10 @@ from paper_2204_14193_b200.synth import field_torch
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 peak = sms * 128 * 1965e6
 frames = field_torch(16, 2160, 3840, seed=9, device="cuda", edges=True)
+only = [int(a) for a in sys.argv[1:]]
 for F, B, border in ((32, 8, 8), (64, 16, 16), (128, 32, 16)):
+    if only and F not in only:
+        continue
     blocks = fse.frames_pattern(16, 2160, 3840, B, 0.05 if B < 32 else 0.04, seed=2)
     plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(B, border, F), iterations=100)
     t = plan.run(frames); torch.cuda.synchronize()

@@ -10,11 +10,12 @@ import paper_2204_14193_b200 as fse
 from paper_2204_14193_b200 import synth
 
 n_frames = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+F = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 H, W = 2160, 3840
 frames = synth.field_torch(n_frames, H, W, 5, "cuda")
-blocks = fse.frames_pattern(n_frames, H, W, 16, 0.05, seed=5)
-plan = fse.ConcealPlan(blocks, H, W, fse.Geometry(B=16, border=16, F=64), rho_hat=0.8, gamma=0.5,
-                       iterations=100)
+blocks = fse.frames_pattern(n_frames, H, W, F // 4, 0.05 if F < 128 else 0.04, seed=5)
+plan = fse.ConcealPlan(blocks, H, W, fse.Geometry(B=F // 4, border=8 if F == 32 else 16, F=F),
+                       rho_hat=0.8, gamma=0.5, iterations=100)
 for _ in range(2):
     tiles, tr = plan.run(frames, trace=True)
 torch.cuda.synchronize()
@@ -43,9 +44,11 @@ for c in np.unique(cta)[:40]:
             ss = sel[slot[sel] == s]
             # nearest iteration start of slot s to t
             d = ((clk[ss] - t + 2**31) & 0xffffffff) - 2**31
+            if d.size == 0:
+                continue
             k = np.argmin(np.abs(d))
             phase.append(float((np.abs(d).flat[k] % per) / per))
-out["block_gap_median"] = float(np.median(gaps))
+out["block_gap_median"] = float(np.median(gaps)) if gaps else None
 out["phase_hist"] = np.histogram(phase, bins=10, range=(0, 1))[0].tolist()
 print(json.dumps(out))
 # phase marks (FSE_TMARK): c[b, j, 0] = T_j - T_0
