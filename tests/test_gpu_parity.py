@@ -388,3 +388,32 @@ def test_frame_sharding_is_bitwise_identical(fse):
             parts.append(plan.run(frames[sh.f0:sh.f1], tile_dtype="f32").cpu().numpy())
             idx.append(sh.index)
         assert np.array_equal(sharding.assemble(parts, idx, len(blocks)), whole), world
+
+
+@pytest.mark.parametrize("dtype,n_frames", [("u8", 520), ("f32", 130)])
+def test_frames_beyond_4gib(fse, dtype, n_frames):
+    """Frame batches larger than 4 GiB (u8: the TMA tensor-map path; f32: the
+    direct loads): blocks in the last frames, whose byte offsets exceed 2^32,
+    conceal exactly as the same blocks of a small batch holding only those
+    frames (64-bit frame addressing end to end)."""
+    import torch
+    from paper_2204_14193_b200.synth import field_torch
+    H, W = 2160, 3840
+    tdt = torch.uint8 if dtype == "u8" else torch.float32
+    big = torch.zeros((n_frames, H, W), dtype=tdt, device="cuda")
+    assert big.numel() * big.element_size() > 2**32
+    pick = [0, n_frames // 2, n_frames - 1]
+    small = field_torch(3, H, W, seed=77, device="cuda", edges=True).to(tdt)
+    for k, f in enumerate(pick):
+        big[f] = small[k]
+    rng = np.random.default_rng(5)
+    n = 40
+    sb = np.stack([rng.integers(0, 3, n), rng.integers(0, H - 16 + 1, n), rng.integers(0, W - 16 + 1, n)],
+                  1).astype(np.int32)
+    bb = sb.copy()
+    bb[:, 0] = np.array(pick, np.int32)[sb[:, 0]]
+    t_big = fse.ConcealPlan(bb, H, W, iterations=100).run(big, tile_dtype="f32").cpu().numpy()
+    t_small = fse.ConcealPlan(sb, H, W, iterations=100).run(small, tile_dtype="f32").cpu().numpy()
+    del big
+    torch.cuda.empty_cache()
+    assert np.array_equal(t_big, t_small)
