@@ -21,6 +21,15 @@ for bf in (100, 200):
             plan.run(frames, t)
         e1.record(); torch.cuda.synchronize()
         s = e0.elapsed_time(e1) / 3 / 1e3
+        # iterations actually run (rFSE stops at the basis target) and the
+        # shared-memory bytes they read: per bin and iteration 8 B of W' (cFSE);
+        # rFSE 16 B of W' (both atoms) + 12 B of criterion coefficients
+        _, tr = plan.run(frames, tile_dtype="f32", trace=True)
+        its = float((tr["uv"][:, :, 0] >= 0).sum(1).double().mean())
+        per_bin = 8 if alg == "cfse" else 28
+        tbps = len(blocks) / s * its * 64 * 64 * per_bin / 1e12
+        peak = torch.cuda.get_device_properties(0).multi_processor_count * 128 * 1965e6 / 1e12
         print(json.dumps({"algorithm": alg, "basis_functions": bf, "blocks": len(blocks),
                           "blocks_per_s": len(blocks) / s, "us_per_block": s / len(blocks) * 1e6,
-                          "plan": plan.info}))
+                          "mean_iterations": its, "smem_bytes_per_bin_iteration": per_bin,
+                          "smem_TBps": tbps, "frac_nominal": tbps / peak, "plan": plan.info}))
