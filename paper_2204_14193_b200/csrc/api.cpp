@@ -527,8 +527,7 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     EncodeTiledFn enc = encode_tiled();
     const char *tma_env = getenv("FSE_TMA");
     const bool tma_default = p->F == 64;  // measured: +1.0 % at F=64, -1.5 % at F=128
-    // (the F = 128 cluster kernel's rounds hold two blocks: direct loads only)
-    if (dtype == FSE_U8 && enc && p->tma_aligned && p->cfg.cluster == 1 &&
+    if (dtype == FSE_U8 && enc && p->tma_aligned &&
         (tma_env ? atoi(tma_env) == 1 : tma_default) &&
         (size_t)a.box_w * a.box_h <= fse::fast_stage_bytes(p->F) && a.box_w <= 256 &&
         a.box_h <= 256 && ((uintptr_t)frames % 16) == 0 && (pitch % 16) == 0 &&

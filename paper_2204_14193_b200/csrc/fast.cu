@@ -27,20 +27,10 @@
 //   F=64 : a = (RPW w + p, lane),           b = a + (0, 32)
 //   F=128: a = (RPW w + p/2, lane+64(p&1)), b = a + (0, 32)
 #include <string.h>
-#include <stdio.h>
-#include <stdlib.h>
 
 #include "common.cuh"
 #include "dft.cuh"
 #include "kernels.h"
-
-#include <cooperative_groups.h>
-
-// F = 128 runs as 2-CTA clusters: each CTA (SM) holds half of two blocks'
-// spectra and interleaves their iterations (see fast_kernel)
-#ifndef FSE_CLUSTER128
-#define FSE_CLUSTER128 0  // measured: 0.85 M vs 1.20 M blocks/s (cross-SM exchange latency)
-#endif
 
 namespace fse {
 
@@ -164,14 +154,10 @@ FSE_DEV void sts128u(unsigned addr, uint4 v) {
                : "memory");
 }
 
-// exchange candidates per slot: two buffers of NW; the F = 128 cluster
-// kernel keeps [block 0/1][parity][8 warps]
-template <int F> constexpr int xch_n() { return F == 128 ? 32 : 2 * FG<F>::NW; }
-// bytes per slot region: [stage] scratch | exchange | red[16] | mbarrier, phase
-// | (F = 128) the two blocks' exchange mbarriers
+// bytes per slot region: [stage] scratch | exchange x 2 | red[16] | mbarrier
 template <int F> constexpr size_t slot_stride(bool tma) {
-  return ((tma ? FG<F>::STAGE : 0) + FG<F>::SCRATCH + xch_n<F>() * sizeof(uint4) + 64 + 16 +
-          (F == 128 ? 16 : 0) + 511) & ~(size_t)511;
+  return ((tma ? FG<F>::STAGE : 0) + FG<F>::SCRATCH + 2 * FG<F>::NW * sizeof(uint4) + 64 + 16 +
+          511) & ~(size_t)511;
 }
 
 // 16-byte shared load at a 32-bit shared-window address (hot loop only)
@@ -224,36 +210,6 @@ template <int F> FSE_DEV void slot_sync(int slot) {
 FSE_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 FSE_DEV void mbar_init(uint64_t *bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-}
-// ---- cluster (distributed shared memory) helpers, F = 128 cluster kernel
-FSE_DEV void mbar_init_n(unsigned addr, unsigned n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(n) : "memory");
-}
-// shared::cluster address of a shared::cta address in CTA `rank` of the cluster
-FSE_DEV unsigned mapa_u32(unsigned addr, unsigned rank) {
-  unsigned r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-FSE_DEV void st_cluster128(unsigned caddr, uint4 v) {
-  asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(caddr), "r"(v.x), "r"(v.y),
-               "r"(v.z), "r"(v.w)
-               : "memory");
-}
-// arrive (release, cluster scope: orders this thread's prior shared stores)
-FSE_DEV void mbar_arrive_cluster(unsigned caddr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
-}
-FSE_DEV void mbar_wait_cluster(unsigned addr, unsigned parity) {
-  unsigned done;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
-        "selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-  } while (!done);
 }
 // one thread: expect `bytes` and start the 3-D tile load (OOB elements -> 0)
 FSE_DEV void tma_window(void *dst, const CUtensorMap *map, uint64_t *bar, unsigned bytes, int x, int y,
@@ -480,16 +436,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     fast_kernel(FastArgs a, int iter_cap, const __grid_constant__ CUtensorMap tmap) {
   typedef FG<F> G;
   static_assert(ALG == 0 || F == 64, "the fused rFSE kernel is built for F = 64");
-  // F = 128 cluster mode (direct loads): a 2-CTA cluster runs rounds of two
-  // blocks; CTA r computes block r's setup FFT and synthesis ("home"), and
-  // its warps 4i..4i+3 hold rows [64 r, 64 r + 64) of block i's spectrum,
-  // so each SM interleaves two independent blocks' iterations (the
-  // single-block F = 128 kernel stalls on every block-wide argmax).  The
-  // argmax candidates of a block's 8 warps meet in both CTAs' shared memory
-  // (local + distributed stores, cluster-scope mbarrier per block).
-  constexpr bool CL = F == 128 && !TMA && ALG == 0 && FSE_CLUSTER128;
-  constexpr int NS = CL ? 2 : KS<F, ALG>::S;  // blocks per round (slots per CTA)
-  namespace cg = cooperative_groups;
+  constexpr int NS = KS<F, ALG>::S;  // blocks (slots) per CTA
   extern __shared__ __align__(16) char smem[];
   char *region = smem;
   float2 *syn_tw = (float2 *)(smem + KS<F, ALG>::REGION);  // exp(+2 pi i j / F), j < F
@@ -502,20 +449,14 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 
   const int tid = threadIdx.x;
   const int slot = tid / G::NT, st = tid - slot * G::NT;
-  const int wphys = st >> 5, lane = st & 31;
-  const unsigned rank = CL ? cg::this_cluster().block_rank() : 0u;
-  // cluster mode: the warp's block (0/1) and its warp index in that block's
-  // row-major layout (rows [16 w, 16 w + 16))
-  const int bw = CL ? wphys >> 2 : 0;
-  const int w = CL ? (int)rank * 4 + (wphys & 3) : wphys;
+  const int w = st >> 5, lane = st & 31;
   char *sb = slots_base + slot * slot_bytes;
   SlotPtrs<F> sp;
   sp.scratch = (float2 *)(sb + STG);
   sp.xch = (uint4 *)(sb + STG + G::SCRATCH);
-  sp.red = (float *)(sp.xch + xch_n<F>());
+  sp.red = (float *)(sp.xch + 2 * G::NW);
   uint64_t *const mbar = (uint64_t *)((char *)sp.red + 64);  // TMA completion barrier
   int *const tphase = (int *)(mbar + 1);                      // its expected phase
-  uint64_t *const xbar = mbar + 2;  // cluster mode: exchange mbarriers of blocks 0, 1
   sp.trace = (float4 *)sp.scratch;  // the FFT scratch holds the trace after setup
   if (a.trace_scratch)  // more iterations than the shared trace holds: per-slot global scratch
     sp.trace = a.trace_scratch + ((size_t)blockIdx.x * NS + slot) * 2 * a.iterations;
@@ -533,16 +474,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if constexpr (CL) {
-    if (tid == 0) {
-      mbar_init_n(smem_u32(xbar), 8);
-      mbar_init_n(smem_u32(xbar + 1), 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    cg::this_cluster().sync();  // the peer's barriers exist before any remote arrive
-  }
   __syncthreads();
-  unsigned xph = 0;  // cluster mode: phase parity of this warp's block exchange
   // issue the TMA load of the support window of this slot's block in round rnd
   auto prefetch = [&](int rnd) {
     if constexpr (!TMA) return;
@@ -560,8 +492,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 #if FSE_DIAG & 32
   unsigned tmk[7];
 #endif
-  for (int round = CL ? blockIdx.x >> 1 : blockIdx.x; round < a.n_rounds;
-       round += CL ? gridDim.x >> 1 : gridDim.x) {
+  for (int round = blockIdx.x; round < a.n_rounds; round += gridDim.x) {
     const int cls = __ldg(a.round_class + round);
     if (cls != loaded) {
       __syncthreads();
@@ -570,13 +501,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       __syncthreads();
       loaded = cls;
     }
-    int b = __ldg(a.rounds + (size_t)round * NS + (CL ? (int)rank : slot));
-    // cluster mode: the block this warp iterates (-1: absent); a CTA whose
-    // home block is absent (odd round) computes its peer's setup again so
-    // both CTAs keep the same barrier sequence, and stores nothing
-    const int bit = CL ? __ldg(a.rounds + (size_t)round * NS + bw) : b;
-    const bool home = !CL || b >= 0;
-    if (CL && !home) b = __ldg(a.rounds + (size_t)round * NS + (int)(rank ^ 1u));
+    const int b = __ldg(a.rounds + (size_t)round * NS + slot);
     if (b < 0) {  // idle this round: keep the slot's prefetch chain going
       if constexpr (TMA) prefetch(round + gridDim.x);
       continue;
@@ -761,20 +686,13 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           S[rm * XS + H] = make_float2(xh.x, -xh.y);
         }
       }
-      const float2 *Sr = S;
-      if constexpr (CL) {
-        cg::this_cluster().sync();  // both CTAs' spectra are complete
-        if (bw != (int)rank) Sr = cg::this_cluster().map_shared_rank(S, bw);
-      } else {
-        slot_sync<F>(slot);
-      }
+      slot_sync<F>(slot);
       // X[r][c] = S[r][c] for c <= F/2, else conj(S[-r][F - c])
       auto bin = [&](int r, int c) -> float2 {
         const bool lo = c <= H;
-        const float2 z = Sr[lo ? r * XS + c : ((F - r) & (F - 1)) * XS + (F - c)];
+        const float2 z = S[lo ? r * XS + c : ((F - r) & (F - 1)) * XS + (F - c)];
         return make_float2(z.x, lo ? z.y : -z.y);
       };
-      if (!CL || bit >= 0) {
 #pragma unroll
       for (int p = 0; p < G::NP; ++p) {
         const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
@@ -785,15 +703,11 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         Rre[p] = __fadd2_rn(make_float2(xa.x, xb.x), make_float2(0.f, 0.f));
         Rim[p] = __fadd2_rn(make_float2(xa.y, xb.y), make_float2(0.f, 0.f));
       }
-      }
     }
     // e0 = sum w s^2 (slot reduction; trace energies only)
     for (int o = 16; o; o >>= 1) e0p += __shfl_xor_sync(0xffffffffu, e0p, o);
-    if (lane == 0) sp.red[wphys] = e0p;
-    if constexpr (CL)
-      cg::this_cluster().sync();  // the peer has read this CTA's spectrum
-    else
-      slot_sync<F>(slot);  // scratch is free from here on (trace area)
+    if (lane == 0) sp.red[w] = e0p;
+    slot_sync<F>(slot);  // scratch is free from here on (trace area)
     FSE_TMARK(4);
 
     // ------------------------------------------------------- iterations
@@ -815,13 +729,9 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     const unsigned kpos = __shfl_sync(0xffffffffu, (unsigned)(rowbase * F) | (unsigned)lane, lane);
     const unsigned tbase =
         __shfl_sync(0xffffffffu, (unsigned)__cvta_generic_to_shared(region), lane);
-    // cluster mode: the shared::cta address of this warp's block exchange
-    // barrier, and the shared::cluster addresses of it in both CTAs
-    const unsigned xbl = CL ? smem_u32(xbar + bw) : 0u;
-    const unsigned xbo = CL ? mapa_u32(xbl, rank) : 0u, xbp = CL ? mapa_u32(xbl, rank ^ 1u) : 0u;
     if constexpr (ALG == 0) {
 #pragma unroll 1
-    for (int it = 0; it < ((CL && bit < 0) ? 0 : a.iterations); ++it) {
+    for (int it = 0; it < a.iterations; ++it) {
 #if FSE_DIAG & 32
       const unsigned clk0 = (unsigned)clock();
 #endif
@@ -924,32 +834,6 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       are = __shfl_sync(0xffffffffu, are, ow);
       aim = __shfl_sync(0xffffffffu, aim, ow);
       gidx = widx;
-      if constexpr (CL) {
-        // the block's 8 candidates, in both CTAs: local + distributed
-        // store, then an arrive on both CTAs' barrier of this block
-        const unsigned par = xph & 1u;
-        const unsigned xa = xc + ((unsigned)bw * 2u + par) * 8u * 16u;
-        if (lane == 0) {
-          const uint4 cand = make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim));
-          sts128u(xa + 16u * (unsigned)w, cand);
-          st_cluster128(mapa_u32(xa + 16u * (unsigned)w, rank ^ 1u), cand);
-          mbar_arrive_cluster(xbo);
-          mbar_arrive_cluster(xbp);
-        }
-        mbar_wait_cluster(xbl, par);
-        xph ^= 1u;
-        uint4 cd[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) cd[j] = lds128u(xa + 16u * (unsigned)j);
-#pragma unroll
-        for (int s = 1; s < 8; s *= 2)
-#pragma unroll
-          for (int j = 0; j + s < 8; j += 2 * s)
-            if (cd[j + s].x > cd[j].x) cd[j] = cd[j + s];
-        gidx = cd[0].y;
-        are = __uint_as_float(cd[0].z);
-        aim = __uint_as_float(cd[0].w);
-      } else
 #if FSE_DIAG & 1
       if (false) {
 #else
@@ -996,8 +880,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       }
       cre = ginv * are;
       cim = ginv * aim;
-      // (cluster mode: the home CTA's first warp of the home block records)
-      if (CL ? (wphys == 4 * (int)rank && lane == 0) : st == 0) {
+      if (st == 0) {
         FSE_CHECK(a.trace_scratch || it < G::TRACE_CAP);
 #if FSE_DIAG & 32
         sp.trace[it] = make_float4(__uint_as_float(gidx), are, aim, __uint_as_float(clk0));
@@ -1129,7 +1012,6 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     }
     slot_sync<F>(slot);
     FSE_TMARK(5);
-    if (CL && !home) continue;  // the peer's block: its home CTA stores it
 
     // ------------------------------------ coefficients, trace, synthesis
     // trace[it] = (index, R_w[u,v]) -> (u | v << 16, c, |R_w[u,v]|^2), and
@@ -1276,7 +1158,6 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       for (int j = 1; j < 7; ++j) ((float *)a.tiles)[(size_t)b * G::B * G::B + j] = (float)(tmk[j] - tmk[0]);
 #endif
   }
-  if constexpr (CL) cg::this_cluster().sync();  // no CTA leaves while its peer may touch its memory
 }
 
 template <int F, int ALG = 0> static size_t fast_smem(int iter_cap) {
@@ -1294,7 +1175,6 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algor
     smem = fast_smem<64, 1>(0);
     if (smem > 227 * 1024) return false;
     cfg->slots = RF_SLOTS;
-    cfg->cluster = 1;
     cfg->threads = KS<64, 1>::CTA;
     cfg->smem_bytes = (int)smem;
     cfg->grid = sm_count;
@@ -1318,8 +1198,7 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algor
       return false;
   }
   if (smem > 227 * 1024) return false;
-  cfg->cluster = F == 128 && FSE_CLUSTER128 ? 2 : 1;
-  cfg->slots = F == 128 && FSE_CLUSTER128 ? 2 : S;  // cluster mode: two blocks per round
+  cfg->slots = S;
   cfg->threads = F == 32 ? FG<32>::CTA : F == 64 ? FG<64>::CTA : FG<128>::CTA;
   cfg->smem_bytes = (int)smem;
   cfg->grid = sm_count;
@@ -1333,35 +1212,10 @@ template <int F, int ALG> static cudaError_t launch_fast_t(const FastArgs &a, co
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        cfg.smem_bytes);
   if (e != cudaSuccess) return e;
-  CUtensorMap none;
-  memset(&none, 0, sizeof none);
-  if (F == 128 && !tmap && cfg.cluster == 2) {
-    // 2-CTA clusters, one round (two blocks) per cluster at a time; as many
-    // clusters as can be co-resident (persistent)
-    cudaLaunchConfig_t lc = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.blockDim = dim3(cfg.threads);
-    lc.dynamicSmemBytes = cfg.smem_bytes;
-    lc.stream = s;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    lc.gridDim = dim3(cfg.grid & ~1);
-    int nclu = 0;
-    e = cudaOccupancyMaxActiveClusters(&nclu, kern, &lc);
-    if (e != cudaSuccess) return e;
-    if (nclu <= 0) return cudaErrorInvalidConfiguration;
-    if (nclu > a.n_rounds) nclu = a.n_rounds;
-    if (nclu <= 0) return cudaSuccess;
-    lc.gridDim = dim3(2 * nclu);
-    if (getenv("FSE_VERBOSE")) fprintf(stderr, "fse: F=128 cluster launch, %d clusters\n", nclu);
-    return cudaLaunchKernelEx(&lc, kern, a, 0, tmap ? *tmap : none);
-  }
   int grid = cfg.grid < a.n_rounds ? cfg.grid : a.n_rounds;
   if (grid <= 0) return cudaSuccess;
+  CUtensorMap none;
+  memset(&none, 0, sizeof none);
   kern<<<grid, cfg.threads, cfg.smem_bytes, s>>>(a, 0, tmap ? *tmap : none);
   return cudaGetLastError();
 }

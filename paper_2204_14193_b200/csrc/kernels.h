@@ -95,7 +95,6 @@ struct FastArgs {
 };
 struct FastConfig {
   int slots, threads, smem_bytes, grid;
-  int cluster;  // CTAs per cluster (F = 128: 2, each round's two blocks span both)
   size_t table_bytes;
   bool global_trace;  // iteration trace kept in global scratch (large I)
 };
