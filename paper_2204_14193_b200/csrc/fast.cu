@@ -175,12 +175,17 @@ FSE_DEV float4 lds128f(unsigned addr) {
 // RA2[r][c] = (-D_a, -D_b) for the pair (r, c), (r, c + 32), c < 32, with
 // the pair selection criterion of bin k written as a quadratic form of
 // a = R_w[k]:  crit = A a.re^2 + C a.im^2 - D a.re a.im  (rfse.py:86-111).
-constexpr int RF_SLOTS = 4;
-constexpr size_t RF_T2_BYTES = 64 * 32 * (sizeof(float4) + sizeof(float2));
+// F = 32: sixteen one-warp blocks per CTA (the rFSE loop state needs up to
+// 128 registers), tables for bins (2p, c), (2p + 1, c) of pair p, column c.
+template <int F> constexpr int rf_slots() { return F == 32 ? 16 : 4; }
+// pair-criterion tables: F^2 / 2 bin pairs x (float4 + float2)
+template <int F> constexpr size_t rf_t2_bytes() {
+  return (size_t)F * F / 2 * (sizeof(float4) + sizeof(float2));
+}
 template <int F, int ALG> struct KS {  // per-algorithm launch shape
-  static constexpr int S = ALG ? RF_SLOTS : FG<F>::S;
+  static constexpr int S = ALG ? rf_slots<F>() : FG<F>::S;
   static constexpr int CTA = FG<F>::NT * S;
-  static constexpr size_t REGION = ALG ? FG<F>::TABLE_BYTES + RF_T2_BYTES : FG<F>::REGION;
+  static constexpr size_t REGION = ALG ? FG<F>::TABLE_BYTES + rf_t2_bytes<F>() : FG<F>::REGION;
 };
 
 FSE_DEV float2 lds64f(unsigned addr) {
@@ -435,7 +440,7 @@ template <int F, bool TMA, int ALG>
 __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     fast_kernel(FastArgs a, int iter_cap, const __grid_constant__ CUtensorMap tmap) {
   typedef FG<F> G;
-  static_assert(ALG == 0 || F == 64, "the fused rFSE kernel is built for F = 64");
+  static_assert(ALG == 0 || F == 32 || F == 64, "the fused rFSE kernel is built for F = 32, 64");
   constexpr int NS = KS<F, ALG>::S;  // blocks (slots) per CTA
   extern __shared__ __align__(16) char smem[];
   char *region = smem;
@@ -904,7 +909,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           lane);
       const unsigned rt2 = __shfl_sync(
           0xffffffffu,
-          (unsigned)__cvta_generic_to_shared(region + G::TABLE_BYTES + 64 * 32 * sizeof(float4)) +
+          (unsigned)__cvta_generic_to_shared(region + G::TABLE_BYTES + F * F / 2 * sizeof(float4)) +
               (unsigned)(rowbase * 32 + lane) * 8u,
           lane);
       unsigned midx = 0;            // bin of the previous pick's second atom
@@ -922,8 +927,9 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         int bp = 0;
 #pragma unroll
         for (int p = 0; p < G::NP; ++p) {
-          const float4 wv = lds128f(tp + (unsigned)(p * F * 16));
-          const float4 wq = lds128f(tq + (unsigned)(p * F * 16));
+          const unsigned po = (unsigned)((F == 32 ? 2 * p : p) * F * 16);  // the pair's table row
+          const float4 wv = lds128f(tp + po);
+          const float4 wq = lds128f(tq + po);
           const float2 wr = make_float2(wv.x, wv.y), wi = make_float2(wv.z, wv.w);
           const float2 qr = make_float2(wq.x, wq.y), qi = make_float2(wq.z, wq.w);
           ffma2_acc(Rre[p], wr, -cre);
@@ -958,10 +964,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         aim = __shfl_sync(0xffffffffu, aim, ow);
         gidx = widx;
         unsigned gkey = wmax;
-        if (lane == 0)
-          sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
-        slot_sync<F>(slot);
-        {
+        if constexpr (G::NW == 2) {
+          if (lane == 0)
+            sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
+          slot_sync<F>(slot);
           const uint4 o = lds128u(xc + 16u * (unsigned)(w ^ 1));
           if (o.x > wmax || (o.x == wmax && o.y < widx)) {
             gidx = o.y;
@@ -969,8 +975,8 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
             are = __uint_as_float(o.z);
             aim = __uint_as_float(o.w);
           }
+          xc ^= (unsigned)(G::NW * sizeof(uint4));
         }
-        xc ^= (unsigned)(G::NW * sizeof(uint4));
         // joint projection of the chosen bin (rfse.py:93-103)
         const unsigned u = gidx >> G::LOG, v = gidx & (F - 1);
         const bool self = ((2 * u) & (F - 1)) == 0 && ((2 * v) & (F - 1)) == 0;
@@ -1169,16 +1175,17 @@ template <int F, int ALG = 0> static size_t fast_smem(int iter_cap) {
 bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algorithm) {
   size_t smem, tb;
   int S;
-  if (algorithm == 1) {  // fused rFSE: F = 64 only
-    if (F != 64) return false;
-    cfg->global_trace = iterations > FG<64>::TRACE_CAP;
-    smem = fast_smem<64, 1>(0);
+  if (algorithm == 1) {  // fused rFSE: F = 32, 64
+    if (F != 32 && F != 64) return false;
+    cfg->global_trace = iterations > (F == 32 ? FG<32>::TRACE_CAP : FG<64>::TRACE_CAP);
+    smem = F == 32 ? fast_smem<32, 1>(0) : fast_smem<64, 1>(0);
     if (smem > 227 * 1024) return false;
-    cfg->slots = RF_SLOTS;
-    cfg->threads = KS<64, 1>::CTA;
+    cfg->slots = F == 32 ? rf_slots<32>() : rf_slots<64>();
+    cfg->threads = F == 32 ? KS<32, 1>::CTA : KS<64, 1>::CTA;
     cfg->smem_bytes = (int)smem;
     cfg->grid = sm_count;
-    cfg->table_bytes = FG<64>::TABLE_BYTES + RF_T2_BYTES;
+    cfg->table_bytes = F == 32 ? FG<32>::TABLE_BYTES + rf_t2_bytes<32>()
+                               : FG<64>::TABLE_BYTES + rf_t2_bytes<64>();
     return true;
   }
   switch (F) {
@@ -1222,7 +1229,10 @@ template <int F, int ALG> static cudaError_t launch_fast_t(const FastArgs &a, co
 
 cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap,
                         cudaStream_t s) {
-  if (a.algorithm == 1) return a.F == 64 ? launch_fast_t<64, 1>(a, cfg, tmap, s) : cudaErrorInvalidValue;
+  if (a.algorithm == 1)
+    return a.F == 64   ? launch_fast_t<64, 1>(a, cfg, tmap, s)
+           : a.F == 32 ? launch_fast_t<32, 1>(a, cfg, tmap, s)
+                       : cudaErrorInvalidValue;
   switch (a.F) {
     case 32: return launch_fast_t<32, 0>(a, cfg, tmap, s);
     case 64: return launch_fast_t<64, 0>(a, cfg, tmap, s);
@@ -1294,7 +1304,7 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       else x1 = W[(r % F) * F + (q + 32) % F];
       T4[i] = make_float4((float)x0.x, (float)x1.x, (float)x0.y, (float)x1.y);
     }
-    if (a.rfse && F == 64) {
+    if (a.rfse && (F == 64 || F == 32)) {
       // rFSE pair tables (rfse.py:40-55, 86-111): the pair criterion
       // 2 (p.re a.re + p.im a.im) with p = [[W00 - W2.re, -W2.im], [-W2.im,
       // W00 + W2.re]] a / Dt, Dt = W00^2 - |W2|^2, W2 = W[2k, 2l], is
@@ -1302,21 +1312,25 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       // C = 2 (W00 + W2.re) / Dt, D = 4 W2.im / Dt; a self-conjugate bin
       // (crit = a.re^2 / W00) has A = 1 / W00, C = D = 0.  Also the minimum of
       // Dt / W00^2 over pair bins.
+      // Entry i = (r, c) of the thread layout (32 columns): bins (r, c) and
+      // (r, c + 32) at F = 64; bins (2r, c) and (2r + 1, c) at F = 32.
       const double w00 = W[0].x;
-      float4 *A4 = (float4 *)(tab + FG<64>::TABLE_BYTES);
-      float2 *A2 = (float2 *)(tab + FG<64>::TABLE_BYTES + 64 * 32 * sizeof(float4));
+      const size_t TB = F == 32 ? FG<32>::TABLE_BYTES : FG<64>::TABLE_BYTES;
+      float4 *A4 = (float4 *)(tab + TB);
+      float2 *A2 = (float2 *)(tab + TB + (size_t)FF / 2 * sizeof(float4));
       double dmin = 1e300;
-      for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
+      for (int i = threadIdx.x; i < FF / 2; i += blockDim.x) {
         const int r = i >> 5, c = i & 31;
         double qa[2], qc[2], qd[2];
         for (int h = 0; h < 2; ++h) {
-          const int cc = c + 32 * h, r2 = (2 * r) % 64, c2 = (2 * cc) % 64;
+          const int br = F == 32 ? 2 * r + h : r, bc = F == 32 ? c : c + 32 * h;
+          const int r2 = (2 * br) % F, c2 = (2 * bc) % F;
           if (r2 == 0 && c2 == 0) {
             qa[h] = 1.0 / w00;
             qc[h] = 0.0;
             qd[h] = 0.0;
           } else {
-            const double2 w2 = W[r2 * 64 + c2];
+            const double2 w2 = W[r2 * F + c2];
             const double d = w00 * w00 - (w2.x * w2.x + w2.y * w2.y);
             dmin = fmin(dmin, d / (w00 * w00));
             qa[h] = 2.0 * (w00 - w2.x) / d;

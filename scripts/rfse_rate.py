@@ -5,13 +5,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2204_14193_b200 as fse
 from paper_2204_14193_b200.synth import field_torch
-nf = 32
+F = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+nf = 32 if F == 64 else 8
 frames = field_torch(nf, 2160, 3840, seed=5, device="cuda", edges=True)
-blocks = fse.frames_pattern(nf, 2160, 3840, 16, 0.05, seed=5)
+blocks = fse.frames_pattern(nf, 2160, 3840, F // 4, 0.05, seed=5)
 for bf in (100, 200):
     for alg in ("cfse", "rfse"):
         kw = dict(iterations=bf) if alg == "cfse" else dict(iterations=bf, basis_target=bf)
-        plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(16, 16, 64), rho_hat=0.8, gamma=0.5,
+        plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(F // 4, F // 4, F), rho_hat=0.8, gamma=0.5,
                                algorithm=alg, **kw)
         t = plan.run(frames)
         torch.cuda.synchronize()
@@ -27,9 +28,9 @@ for bf in (100, 200):
         _, tr = plan.run(frames, tile_dtype="f32", trace=True)
         its = float((tr["uv"][:, :, 0] >= 0).sum(1).double().mean())
         per_bin = 8 if alg == "cfse" else 28
-        tbps = len(blocks) / s * its * 64 * 64 * per_bin / 1e12
+        tbps = len(blocks) / s * its * F * F * per_bin / 1e12
         peak = torch.cuda.get_device_properties(0).multi_processor_count * 128 * 1965e6 / 1e12
-        print(json.dumps({"algorithm": alg, "basis_functions": bf, "blocks": len(blocks),
+        print(json.dumps({"F": F, "algorithm": alg, "basis_functions": bf, "blocks": len(blocks),
                           "blocks_per_s": len(blocks) / s, "us_per_block": s / len(blocks) * 1e6,
                           "mean_iterations": its, "smem_bytes_per_bin_iteration": per_bin,
                           "smem_TBps": tbps, "frac_nominal": tbps / peak, "plan": plan.info}))

@@ -17,8 +17,8 @@ def fse(cuda_ok):
     return fse
 
 
-def _plans(fse, blocks, H, W, **kw):
-    geo = fse.Geometry(16, 16, 64)
+def _plans(fse, blocks, H, W, geo=None, **kw):
+    geo = geo or fse.Geometry(16, 16, 64)
     fast = fse.ConcealPlan(blocks, H, W, geo, rho_hat=0.8, gamma=0.5, algorithm="rfse",
                            precision="fp32", **kw)
     ref = fse.ConcealPlan(blocks, H, W, geo, rho_hat=0.8, gamma=0.5, algorithm="rfse",
@@ -130,3 +130,88 @@ def test_fused_rfse_random_geometry(fse, seed):
     t64 = ref.run(fr, tile_dtype="f64")
     dev = float((t32.double() - t64).abs().max())
     assert dev <= 0.5, (seed, H, W, dtype, iters, bt, dev)
+
+
+# ---------------------------------------------------------------- F = 32
+
+
+@pytest.mark.parametrize("dtype,iters,bt", [("u8", 50, None), ("f32", 40, 37), ("u8", 100, 60)])
+def test_fused_rfse32_matches_fp64(fse, dtype, iters, bt):
+    """The F = 32 fused rFSE (one warp per block, pair entries (2p, c),
+    (2p + 1, c)) against the fp64 rFSE plan: max |dpx| <= 0.5, canonical
+    members, tally rule."""
+    import torch
+    from paper_2204_14193_b200.synth import field_torch
+    H, W = 200, 320
+    frames = field_torch(2, H, W, seed=23, device="cuda", edges=True)
+    if dtype != "u8":
+        frames = frames.to(torch.float32)
+    blocks = fse.frames_pattern(2, H, W, 8, 0.06, seed=8)
+    blocks = np.concatenate([blocks, np.array([[0, 0, 0], [0, 0, W - 8], [1, H - 8, 0],
+                                               [1, H - 8, W - 8]], np.int32)])
+    kw = dict(iterations=iters) if bt is None else dict(iterations=iters, basis_target=bt)
+    fast, ref = _plans(fse, blocks, H, W, geo=fse.Geometry(8, 8, 32), **kw)
+    t32, tr = fast.run(frames, tile_dtype="f32", trace=True)
+    t64 = ref.run(frames, tile_dtype="f64")
+    dev = (t32.double() - t64).abs().reshape(len(blocks), -1).max(1).values.cpu().numpy()
+    assert dev.max() <= 0.5, (dev.max(), int((dev > 0.5).sum()))
+    uv = tr["uv"].cpu().numpy()
+    for k in range(len(blocks)):
+        used = uv[k, :, 0] >= 0
+        u, v = uv[k, used, 0], uv[k, used, 1]
+        mu, mv = (-u) % 32, (-v) % 32
+        assert np.all(u * 32 + v <= mu * 32 + mv)
+        selfc = ((2 * u) % 32 == 0) & ((2 * v) % 32 == 0)
+        tally = int(np.sum(np.where(selfc, 1, 2)))
+        if bt is None:
+            assert used.sum() == fast.iterations
+        else:
+            assert tally >= bt and tally - (1 if selfc[-1] else 2) < bt
+
+
+def test_fused_rfse32_selection_sequence(fse):
+    """F = 32 fused canonical (u, v) sequence equals the reference-arithmetic
+    per-window rFSE's on interior windows, up to the first near-tie."""
+    import torch
+    from paper_2204_14193_b200.synth import frame_u8
+    from tests._windows import window_of
+    fr = frame_u8(160, 224, seed=4)
+    blocks = np.array([[0, 32 + 24 * i, 32 + 40 * j] for i in range(3) for j in range(4)], np.int32)
+    fast, _ = _plans(fse, blocks, 160, 224, geo=fse.Geometry(8, 8, 32), iterations=40)
+    _, tr = fast.run(torch.from_numpy(fr).cuda(), tile_dtype="f32", trace=True)
+    uv = tr["uv"].cpu().numpy()
+    full = 0
+    for k, (f, t, l) in enumerate(blocks):
+        s, lab = window_of(fr.astype(np.float64), t, l, 32, 8, 8)
+        r = fse.extrapolate_rfse(s, fse.AreaMask(lab), fse.FseConfig(
+            rho_hat=0.8, gamma=0.5, iterations=40, fft_dims=(32, 32), algorithm="rfse"))
+        ref_uv = np.array([rec.frequency for rec in r.trace])
+        same = np.all(ref_uv == uv[k], axis=1)
+        first_diff = len(same) if same.all() else int(np.argmin(same))
+        assert first_diff >= 15, (k, first_diff)
+        full += first_diff == len(same)
+    assert full >= len(blocks) // 2
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fused_rfse32_random_geometry(fse, seed):
+    import torch
+    from paper_2204_14193_b200.synth import field
+    rng = np.random.default_rng(4000 + seed)
+    H, W = int(rng.integers(12, 120)), int(rng.integers(12, 120))
+    n = int(rng.integers(6, 20))
+    blocks = np.stack([np.zeros(n, np.int64), rng.integers(0, H - 8 + 1, n),
+                       rng.integers(0, W - 8 + 1, n)], 1).astype(np.int32)
+    img = field(H, W, seed=seed)
+    if seed % 2 == 0:
+        img = np.clip(np.rint(img), 0, 255).astype(np.uint8)
+    iters = int(rng.choice([1, 9, 40]))
+    bt = None if rng.random() < 0.5 else int(rng.integers(1, 2 * iters + 1))
+    kw = dict(iterations=iters) if bt is None else dict(iterations=iters, basis_target=bt)
+    try:
+        fast, ref = _plans(fse, blocks, H, W, geo=fse.Geometry(8, 8, 32), **kw)
+    except fse.ConfigError:
+        pytest.skip("degenerate pair geometry for this random image")
+    fr = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    dev = float((fast.run(fr, tile_dtype="f32").double() - ref.run(fr, tile_dtype="f64")).abs().max())
+    assert dev <= 0.5, (seed, H, W, iters, bt, dev)
