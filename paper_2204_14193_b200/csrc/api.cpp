@@ -417,15 +417,32 @@ int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int 
   if (nc) CK(cudaMemcpyAsync(p->inv_w00, inv.data(), nc * sizeof(float), cudaMemcpyHostToDevice, st));
 
   if (p->fast) {
-    // rounds of `slots` same-class blocks, grouped by class
+    // rounds of `slots` same-class blocks, grouped by class.  A batch too
+    // small to fill every slot of every SM is spread: the fewest blocks per
+    // round (the other slots idle) whose rounds still fit one wave of
+    // persistent CTAs, so the blocks share SMs less and finish sooner
+    // (config 2, 256 blocks: 165 -> 108 us; FSE_SPREAD=0 packs full rounds).
     const int Sl = p->cfg.slots;
     std::vector<std::vector<int32_t>> by(nc);
     for (int b = 0; b < n_blocks; ++b) by[bclass[b]].push_back(b);
+    int use = Sl;
+    const char *spread_env = getenv("FSE_SPREAD");
+    if (!spread_env || atoi(spread_env) != 0) {
+      const int ctas = std::max(1, p->cfg.grid);
+      for (int u = 1; u < Sl; ++u) {
+        long r = 0;
+        for (int c = 0; c < nc; ++c) r += ((long)by[c].size() + u - 1) / u;
+        if (r <= ctas) {
+          use = u;
+          break;
+        }
+      }
+    }
     std::vector<int32_t> rounds, rcls;
     for (int c = 0; c < nc; ++c) {
       const auto &v = by[c];
-      for (size_t i = 0; i < v.size(); i += Sl) {
-        for (int s = 0; s < Sl; ++s) rounds.push_back(i + s < v.size() ? v[i + s] : -1);
+      for (size_t i = 0; i < v.size(); i += use) {
+        for (int s = 0; s < Sl; ++s) rounds.push_back(s < use && i + s < v.size() ? v[i + s] : -1);
         rcls.push_back(c);
       }
     }
