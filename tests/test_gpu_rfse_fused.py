@@ -215,3 +215,31 @@ def test_fused_rfse32_random_geometry(fse, seed):
     fr = torch.from_numpy(np.ascontiguousarray(img)).cuda()
     dev = float((fast.run(fr, tile_dtype="f32").double() - ref.run(fr, tile_dtype="f64")).abs().max())
     assert dev <= 0.5, (seed, H, W, iters, bt, dev)
+
+
+@pytest.mark.parametrize("F", [32, 64])
+def test_fused_rfse_tma_matches_direct(fse, F):
+    """rFSE instantiations with TMA window staging (forced, FSE_TMA=1) and
+    direct loads (FSE_TMA=0) give identical tiles and traces; the blocks sit
+    where every window box starts 16-byte aligned (TMA-legal)."""
+    import os
+    import torch
+    from paper_2204_14193_b200.synth import field_torch
+    B = F // 4
+    H, W = 256, 448
+    frames = field_torch(2, H, W, seed=91, device="cuda", edges=True)
+    rng = np.random.default_rng(F)
+    n = 40
+    left = 16 * rng.integers(0, (W - B) // 16, n) + (8 if F == 32 else 0)
+    blocks = np.stack([rng.integers(0, 2, n), rng.integers(0, H - B + 1, n), left], 1).astype(np.int32)
+    plan, _ = _plans(fse, blocks, H, W, geo=fse.Geometry(B, B, F), iterations=50, basis_target=60)
+    out = {}
+    try:
+        for v in ("0", "1"):
+            os.environ["FSE_TMA"] = v
+            t, tr = plan.run(frames, tile_dtype="f32", trace=True)
+            out[v] = (t.cpu().numpy(), tr["uv"].cpu().numpy(), tr["c"].cpu().numpy())
+    finally:
+        del os.environ["FSE_TMA"]
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
