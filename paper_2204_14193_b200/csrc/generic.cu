@@ -185,6 +185,105 @@ __device__ void cfse_iterate(Cplx<T> *R, const Cplx<T> *W, int M, int N, T gamma
   __syncthreads();
 }
 
+// cfse_iterate with the residual spectrum in registers (windows of up to
+// kGenThreads * BPT bins: every size up to 64 x 64): thread t owns bins
+// t + kGenThreads j, j < BPT, in the same increasing order as the shared-
+// memory loop, so per-thread first maxima, the block reduction and every
+// IEEE op are identical (bit-exact); only W' is read from shared memory.
+// The winner's residual value travels with the reduction, so one barrier
+// per iteration publishes (value, index).
+template <typename T>
+__device__ void argmax_combine_v(T &v, int &i, T &re, T &im, T v2, int i2, T re2, T im2) {
+  if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; re = re2; im = im2; }
+}
+
+template <typename T, int BPT>
+__device__ void cfse_iterate_reg(const Cplx<T> *R0, const Cplx<T> *W, int M, int N, T gamma,
+                                 T inv_w00, int iterations, double e0, int64_t *us, int64_t *vs,
+                                 double *cs, double *es, double *red) {
+  typedef Ieee<T> F;
+  static_assert(kGenThreads / 32 * 2 * sizeof(double2) <= 64 * sizeof(double), "winner slots");
+  const int MN = M * N, tid = threadIdx.x;
+  // the warp winners: (value re, im) and (|R|^2, index), 16 warps
+  double2 *wa = (double2 *)red, *wb = wa + kGenThreads / 32;
+  const T damp = F::mul(gamma, F::sub((T)2.0, gamma));
+  T e = (T)e0;
+  Cplx<T> R[BPT];
+  int kk[BPT], ll[BPT];
+  T best = (T)-1.0, bre = (T)0.0, bim = (T)0.0;
+  int bi = 0;
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {  // pass 0: load + scan
+    const int i = tid + kGenThreads * j;
+    kk[j] = i / N;
+    ll[j] = i - kk[j] * N;
+    if (i < MN) {
+      R[j] = R0[i];
+      T m2 = F::add(F::mul(R[j].re, R[j].re), F::mul(R[j].im, R[j].im));
+      if (m2 > best) { best = m2; bi = i; bre = R[j].re; bim = R[j].im; }
+    }
+  }
+  const int w = tid >> 5, lane = tid & 31;
+  for (int it = 0; it < iterations; ++it) {
+    for (int o = 16; o; o >>= 1) {
+      const T v2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      const T r2 = __shfl_xor_sync(0xffffffffu, bre, o), m2 = __shfl_xor_sync(0xffffffffu, bim, o);
+      argmax_combine_v(best, bi, bre, bim, v2, i2, r2, m2);
+    }
+    if (lane == 0) {
+      wa[w] = make_double2((double)bre, (double)bim);
+      wb[w] = make_double2((double)best, __longlong_as_double((long long)bi));
+    }
+    __syncthreads();
+    // every thread merges the 16 warp winners with the same total order
+    // (larger |R|^2, then smaller index)
+    T bv = (T)wb[0].x, ar = (T)wa[0].x, ai = (T)wa[0].y;
+    int bidx = (int)__double_as_longlong(wb[0].y);
+#pragma unroll 4
+    for (int q = 1; q < kGenThreads / 32; ++q) {
+      const double2 ca = wa[q], cb = wb[q];
+      argmax_combine_v(bv, bidx, ar, ai, (T)cb.x, (int)__double_as_longlong(cb.y), (T)ca.x, (T)ca.y);
+    }
+    const int idx = bidx;
+    const int u = idx / N, v = idx - u * N;
+    const T cr = F::mul(F::mul(gamma, ar), inv_w00);
+    const T ci = F::mul(F::mul(gamma, ai), inv_w00);
+    if (tid == 0) {
+      T m2 = F::add(F::mul(ar, ar), F::mul(ai, ai));
+      e = F::sub(e, F::mul(F::mul(damp, m2), inv_w00));
+      us[it] = u;
+      vs[it] = v;
+      cs[2 * it] = (double)cr;
+      cs[2 * it + 1] = (double)ci;
+      es[it] = (double)e;
+    }
+    if (it + 1 == iterations) break;
+    best = (T)-1.0;
+    bi = 0;
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const int i = tid + kGenThreads * j;
+      if (i < MN) {
+        int ks = kk[j] - u, ls = ll[j] - v;
+        if (ks < 0) ks += M;
+        if (ls < 0) ls += N;
+        const Cplx<T> wv = W[ks * N + ls];
+        Cplx<T> x = R[j];
+        T pr = F::sub(F::mul(cr, wv.re), F::mul(ci, wv.im));
+        T pi = F::add(F::mul(cr, wv.im), F::mul(ci, wv.re));
+        x.re = F::sub(x.re, pr);
+        x.im = F::sub(x.im, pi);
+        R[j] = x;
+        T m2 = F::add(F::mul(x.re, x.re), F::mul(x.im, x.im));
+        if (m2 > best) { best = m2; bi = i; bre = x.re; bim = x.im; }
+      }
+    }
+    __syncthreads();  // winner slots reuse
+  }
+  __syncthreads();
+}
+
 // rFSE loop (rfse.py:58-167): per iteration a scan of every bin with the
 // joint projection onto the conjugate pair {phi, conj(phi)} (variable
 // denominators D = w00^2 - |W[2k,2l]|^2, self-conjugate bins on their own
@@ -427,7 +526,9 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     __syncthreads();
   }
   int n_it = a.iterations;
-  if (ALG == 0) {
+  if (ALG == 0 && MN <= kGenThreads * 8) {
+    cfse_iterate_reg<T, 8>(R, Wt, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, red);
+  } else if (ALG == 0) {
     cfse_iterate<T>(R, Wt, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, nullptr,
                     (T *)red, redi, bcast);
   } else {
@@ -446,7 +547,8 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     double gr = 0.0, gi = 0.0;
     for (int it = 0; it < n_it; ++it) {
       int u = (int)us[it], v = (int)vs[it];
-      double2 p = twMp[(int)(((long long)u * m) % M)], q = twNp[(int)(((long long)v * n) % N)];
+      // (u, m < M <= 4096: the products fit 32 bits)
+      double2 p = twMp[(u * m) % M], q = twNp[(v * n) % N];
       double pr = p.x * q.x - p.y * q.y, pi = p.x * q.y + p.y * q.x;
       double cr = cs[2 * it], ci = cs[2 * it + 1];
       gr += cr * pr - ci * pi;
