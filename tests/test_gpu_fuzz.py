@@ -37,7 +37,8 @@ def _case(seed):
     return F, B, border, H, W, n_frames, str(dtype), iters, blocks
 
 
-@pytest.mark.parametrize("seed", range(24))
+# FSE_FUZZ_SEEDS widens the sweep for one-off robustness runs (default 24)
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("FSE_FUZZ_SEEDS", 24))))
 def test_fused_path_random_geometry(fse, seed):
     import torch
     from paper_2204_14193_b200.synth import field

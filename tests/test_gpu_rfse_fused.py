@@ -101,7 +101,43 @@ def test_rfse_degenerate_support_raises(fse):
         fse.extrapolate_rfse(np.random.default_rng(0).random((32, 32)) * 255, fse.AreaMask(lab), cfg)
 
 
-@pytest.mark.parametrize("seed", range(6))
+_SEEDS = int(__import__("os").environ.get("FSE_FUZZ_SEEDS", 0))  # widen for one-off sweeps
+
+
+def _rfse_gate(fse, img, blocks, t32, tr32, t64, F, B, iters, bt):
+    """fp32 gate for rFSE (as for cFSE): every block within 0.5
+    gray levels of the fp64 plan, except certified near-ties.  A block is
+    certified when its canonical selection sequence equals the per-window
+    reference-arithmetic rFSE's (fp64) up to a first divergence k >= 1 at
+    which the fp32 run's own energy decrease for its pick is within 1e-4
+    (relative) of the fp64 run's decrease for the fp64 pick -- both picks
+    are greedy-optimal to fp32 accumulated precision."""
+    from tests._windows import window_of
+    dev = (t32.double() - t64).abs().reshape(len(blocks), -1).max(1).values.cpu().numpy()
+    uv = tr32["uv"].cpu().numpy()
+    e32 = tr32["e"].cpu().numpy().astype(np.float64)
+    certified = []
+    for k in np.nonzero(dev > 0.5)[0]:
+        f, t, l = (int(x) for x in blocks[k])
+        fr = img[f] if img.ndim == 3 else img
+        s, lab = window_of(fr.astype(np.float64), t, l, F, B, B)
+        r = fse.extrapolate_rfse(s, fse.AreaMask(lab), fse.FseConfig(
+            rho_hat=0.8, gamma=0.5, iterations=iters, fft_dims=(F, F), algorithm="rfse", basis_target=bt))
+        ref_uv = np.array([rec.frequency for rec in r.trace])
+        e64 = np.array([rec.residual_energy for rec in r.trace])
+        m = min(len(ref_uv), int((uv[k, :, 0] >= 0).sum()))
+        same = np.all(ref_uv[:m] == uv[k, :m], axis=1)
+        assert not same.all(), (k, "identical selections but pixels differ", dev[k])
+        d = int(np.argmin(same))
+        assert d >= 1, (k, "diverges at the first selection", dev[k])
+        dec32, dec64 = e32[k, d - 1] - e32[k, d], e64[d - 1] - e64[d]
+        assert abs(dec32 - dec64) <= 1e-4 * abs(dec64), (k, d, dec32, dec64, dev[k])
+        certified.append((int(k), d, float(dev[k])))
+    assert len(certified) <= max(1, len(blocks) // 50), certified
+    return certified
+
+
+@pytest.mark.parametrize("seed", range(_SEEDS or 6))
 def test_fused_rfse_random_geometry(fse, seed):
     """Random image sizes (clipped windows), positions, frame types and
     iteration budgets: fused fp32 rFSE within 0.5 gray levels of fp64."""
@@ -126,10 +162,10 @@ def test_fused_rfse_random_geometry(fse, seed):
     except fse.ConfigError:
         pytest.skip("degenerate pair geometry for this random image")
     fr = torch.from_numpy(np.ascontiguousarray(img)).cuda()
-    t32 = fast.run(fr, tile_dtype="f32")
+    t32, tr32 = fast.run(fr, tile_dtype="f32", trace=True)
     t64 = ref.run(fr, tile_dtype="f64")
-    dev = float((t32.double() - t64).abs().max())
-    assert dev <= 0.5, (seed, H, W, dtype, iters, bt, dev)
+    cert = _rfse_gate(fse, img, blocks, t32, tr32, t64, 64, 16, iters, bt)
+    print(seed, H, W, dtype, iters, bt, "certified near-ties:", cert)
 
 
 # ---------------------------------------------------------------- F = 32
@@ -193,7 +229,7 @@ def test_fused_rfse32_selection_sequence(fse):
     assert full >= len(blocks) // 2
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(_SEEDS or 4))
 def test_fused_rfse32_random_geometry(fse, seed):
     import torch
     from paper_2204_14193_b200.synth import field
@@ -213,8 +249,10 @@ def test_fused_rfse32_random_geometry(fse, seed):
     except fse.ConfigError:
         pytest.skip("degenerate pair geometry for this random image")
     fr = torch.from_numpy(np.ascontiguousarray(img)).cuda()
-    dev = float((fast.run(fr, tile_dtype="f32").double() - ref.run(fr, tile_dtype="f64")).abs().max())
-    assert dev <= 0.5, (seed, H, W, iters, bt, dev)
+    t32, tr32 = fast.run(fr, tile_dtype="f32", trace=True)
+    t64 = ref.run(fr, tile_dtype="f64")
+    cert = _rfse_gate(fse, img, blocks, t32, tr32, t64, 32, 8, iters, bt)
+    print(seed, H, W, iters, bt, "certified near-ties:", cert)
 
 
 @pytest.mark.parametrize("F", [32, 64])
