@@ -64,7 +64,7 @@ def test_fused_path_random_geometry(fse, seed):
     print(seed, F, B, border, H, W, nf, dtype, iters, len(blocks), st)
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("FSE_FUZZ_SEEDS", 6))))
 def test_fp64_plan_random_geometry(fse, seed):
     """The fp64 image-level path (reference arithmetic, any window size) on
     random geometry: tiles within 1e-9 of the fp64 oracle."""
