@@ -18,7 +18,10 @@
  *   FSE_ERR_CUDA         -> CUDA runtime failure
  *
  * All entry points are reentrant; launches are asynchronous on `stream`
- * unless stated.  Multi-GPU = one call per device (the caller sets the
+ * unless stated.  A plan owns device scratch (generic-path windows, the
+ * fused path's global trace for large I), so one plan serves one run at a
+ * time: runs of the same plan on different streams must be ordered by the
+ * caller; distinct plans are independent.  Multi-GPU = one call per device (the caller sets the
  * current device), no collective is involved.
  */
 #ifndef FSE_B200_H
