@@ -43,6 +43,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> s
     cmd = [nvcc(), *ARCH, *[f"-D{d}" for d in defines], "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-I", os.path.join(REPO, "include"),
            "-o", target + ".tmp", *[os.path.join(HERE, s) for s in SOURCES]]
+    if out is not None:  # diagnostic variants may try other code-generation flags
+        cmd[1:1] = os.environ.get("FSE_NVCC_EXTRA", "").split()
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
