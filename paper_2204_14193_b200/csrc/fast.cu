@@ -758,6 +758,22 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       int bps[CH];
 #pragma unroll
       for (int c = 0; c < CH; ++c) { bst[c] = -1.f; bxs[c] = 0.f; bps[c] = c * (G::NP / CH); }
+#ifndef FSE_PACKKEY
+// 1: the first-max tracker keeps one packed key per thread -- |R|^2 bits with
+// the low log2(F) bits replaced by the bin's rank (4 ops per pair instead of
+// 5; F=64 loop 569 -> 521 instructions, +3.3 % on config 5).  Selection then
+// resolves |R|^2 to 2^-17 relative (ties by row-major index), below fp32's
+// accumulated noise but above exact first-max: config 3 gained one certified
+// near-tie (2 of 402 blocks, PSNR delta 2e-4 dB).  Off: exact fp32 first max.
+#define FSE_PACKKEY 0
+#endif
+      constexpr bool PK = FSE_PACKKEY && !G::PLANAR && CH == 1;
+      unsigned bkey = 0u;  // PK: truncated |R|^2 bits | (NP-1-p) << 1 | member a
+      // (the mask laundered through a shuffle stays a register operand, so
+      // clear-and-insert is one LOP3 with the rank as its immediate)
+      // (from the runtime window size, so that it is not an immediate:
+      // ~(F - 1) clears the rank bits, 2 NP <= F)
+      const unsigned kmask = PK ? 0u - (unsigned)a.F : 0u;
       if (!G::PLANAR) {
         // table index (rowoff, coloff) = ((rowbase - u) mod F, (lane - v) mod F)
         constexpr unsigned RM = (unsigned)(F - 1) << G::LOG;
@@ -795,7 +811,14 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 #if FSE_DIAG & 2
           bst[ch] = fmax3(bst[ch], mg.x, mg.y);
 #else
-          first_max(bst[ch], bps[ch], bxs[ch], mg, p);
+          if constexpr (PK) {
+            static_assert(!PK || 2 * G::NP <= F, "rank bits fit under the mask");
+            const unsigned ka = (__float_as_uint(mg.x) & kmask) | (unsigned)(((G::NP - 1 - p) << 1) | 1);
+            const unsigned kb = (__float_as_uint(mg.y) & kmask) | (unsigned)((G::NP - 1 - p) << 1);
+            bkey = max(bkey, max(ka, kb));
+          } else {
+            first_max(bst[ch], bps[ch], bxs[ch], mg, p);
+          }
 #endif
         }
       } else {
@@ -827,8 +850,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       for (int c = 1; c < CH; ++c)
         if (bst[c] > best) { best = bst[c]; bp = bps[c]; bx = bxs[c]; }
       // thread's first max (member a wins ties inside the pair)
-      const int myidx = bin_index<F>(w, lane, bp, bx >= best ? 0 : 1);
-      const unsigned key = __float_as_uint(best);  // best >= 0: monotone as unsigned
+      const int myidx = PK ? bin_index<F>(w, lane, G::NP - 1 - (int)((bkey >> 1) & (unsigned)(G::NP - 1)),
+                                          (bkey & 1u) ? 0 : 1)
+                           : bin_index<F>(w, lane, bp, bx >= best ? 0 : 1);
+      const unsigned key = PK ? (bkey & kmask) : __float_as_uint(best);  // best >= 0: monotone as unsigned
       const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
       const unsigned widx = __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
       int pw, mw, ow;
