@@ -281,3 +281,27 @@ def test_fused_rfse_tma_matches_direct(fse, F):
         del os.environ["FSE_TMA"]
     for a, b in zip(out["0"], out["1"]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("F", [32, 64])
+def test_fused_rfse_global_trace(fse, F):
+    """More iterations than the shared-memory trace holds (F=32: 136, F=64:
+    400): the per-slot global trace path, against the fp64 plan."""
+    import torch
+    from paper_2204_14193_b200.synth import field
+    B = F // 4
+    H, W = 3 * F, 4 * F
+    img = field(H, W, seed=F + 1)
+    rng = np.random.default_rng(F)
+    n = 12
+    blocks = np.stack([np.zeros(n, np.int64), rng.integers(0, H - B + 1, n),
+                       rng.integers(0, W - B + 1, n)], 1).astype(np.int32)
+    iters = 450 if F == 64 else 300
+    fast, ref = _plans(fse, blocks, H, W, geo=fse.Geometry(B, B, F), iterations=iters,
+                       basis_target=iters + 100)
+    assert fast.info["fast_path"] == 1
+    fr = torch.from_numpy(img).cuda()
+    t32, tr32 = fast.run(fr, tile_dtype="f32", trace=True)
+    t64 = ref.run(fr, tile_dtype="f64")
+    cert = _rfse_gate(fse, img, blocks, t32, tr32, t64, F, B, iters, iters + 100)
+    print(F, "certified near-ties:", cert)
