@@ -286,7 +286,8 @@ def main():
         host = frames.cpu().pin_memory()
         con = fse.Concealer(blocks, nf, cfg["H"], cfg["W"], geo, rho_hat=RHO, gamma=GAMMA,
                             iterations=cfg["iters"], precision="fp32",
-                            chunk_frames=int(os.environ.get("FSE_CHUNK_FRAMES", 8)))
+                            chunk_frames=(int(os.environ["FSE_CHUNK_FRAMES"])
+                                          if os.environ.get("FSE_CHUNK_FRAMES") else None))
         for _ in range(max(1, a.warmup)):
             con.run(host)
         if dist:
