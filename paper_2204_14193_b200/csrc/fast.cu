@@ -26,6 +26,17 @@
 //   F=32 : a = (2p, lane),                  b = (2p+1, lane)
 //   F=64 : a = (RPW w + p, lane),           b = a + (0, 32)
 //   F=128: a = (RPW w + p/2, lane+64(p&1)), b = a + (0, 32)
+//
+// Compile-time knobs (defaults = the measured best on config 5; each was
+// A/B-measured with scripts/gpu_ab.sh, results in DESIGN.md section 4):
+//   FSE_BPT64 / FSE_BPT128  bins per thread at F=64 / 128 (64 / 64)
+//   FSE_SLOTS64 / FSE_SLOTS32  blocks per CTA at F=64 / 32 (6 / 20)
+//   FSE_PREFETCH            W' loads issued this many pairs ahead (2)
+//   FSE_CHAINS64 / FSE_CHAINS128  independent first-max chains (1 / 1)
+//   FSE_XTREE               F=128 warp-candidate merge in registers (1)
+//   FSE_MAX3 / FSE_PACKKEY  alternative first-max trackers (0 / 0)
+//   FSE_DIAG                diagnostic builds (bit 32: per-phase clock probe)
+//   FSE_CHECKS              device asserts on every shared/global index
 #include <string.h>
 
 #include "common.cuh"
