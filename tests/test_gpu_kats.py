@@ -85,3 +85,31 @@ def test_fused_plan_constant_frame(fse):
     assert plan.info["fast_path"] == 1
     t = plan.run(frames, tile_dtype="f32").cpu().numpy()
     np.testing.assert_allclose(t, 200.0, rtol=0, atol=1e-3)
+
+
+def test_concurrent_calls(fse):
+    """every function is pure, so concurrent calls on distinct
+    arrays are safe -- four threads calling extrapolate_cfse / _rfse at once
+    give the sequential results bit for bit."""
+    import threading
+    from paper_2204_14193_b200.synth import field
+    m = _mask(fse)
+    sigs = [field(64, 64, seed=40 + k) for k in range(8)]
+    cc = fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=40)
+    rc = fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=20, algorithm="rfse")
+    want = [(fse.extrapolate_cfse(s, m, cc).reconstructed, fse.extrapolate_rfse(s, m, rc).reconstructed)
+            for s in sigs]
+    got = [None] * len(sigs)
+
+    def work(k):
+        for j in range(k, len(sigs), 4):
+            got[j] = (fse.extrapolate_cfse(sigs[j], m, cc).reconstructed,
+                      fse.extrapolate_rfse(sigs[j], m, rc).reconstructed)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for (a, b), (c, d) in zip(want, got):
+        assert np.array_equal(a, c) and np.array_equal(b, d)
