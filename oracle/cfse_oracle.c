@@ -17,6 +17,8 @@
  *   orc_extrapolate     <- cfse.py:28-52,110-142 (_prepare + extrapolate_cfse)
  *   orc_conceal_blocks  <- SPEC.md:332-340       (harness `conceal`: centred
  *                          F x F window, valid_rect = image, write Re{g})
+ *   orc_loss_pattern    <- SURVEY.md 8(d)        (seeded isolated-block loss
+ *                          selection; the bench's reference-arm block list)
  *
  * Arithmetic order in orc_cfse_kernel follows the numba loop exactly with
  * no FMA contraction (compile with -ffp-contract=off): c = (gamma*a)*inv_w00,
@@ -320,6 +322,57 @@ int orc_conceal_blocks(const void *frames, int dtype, int H, int Wd,
     free(s); free(rec); free(lab); free(us); free(vs); free(cs); free(es);
   }
   return err;
+}
+
+/* ---------------------------------------------------- loss pattern */
+
+/* Seeded isolated-block loss selection of SURVEY.md 8(d) (the same
+ * generator the product's fse_loss_pattern implements, restated here so
+ * the reference arm of bench.py builds its block list without the product
+ * library): Fisher-Yates shuffle of the (H/B) x (W/B) block grid driven by
+ * splitmix64(seed), then random-sequential selection rejecting any block
+ * 8-adjacent to one already chosen, up to `count` blocks; output sorted
+ * row-major as (top, left) pairs.  Returns the number selected. */
+static uint64_t orc_splitmix64(uint64_t *x) {
+  uint64_t z = (*x += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static int orc_cmp_pair(const void *a, const void *b) {
+  const int32_t *x = (const int32_t *)a, *y = (const int32_t *)b;
+  if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+  return x[1] < y[1] ? -1 : (x[1] > y[1]);
+}
+
+int orc_loss_pattern(int H, int W, int B, int count, uint64_t seed, int32_t *top_left) {
+  if (H < 1 || W < 1 || B < 1 || count < 0) return -1;
+  int gh = H / B, gw = W / B, n = gh * gw, k = 0;
+  int32_t *perm = (int32_t *)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
+  uint8_t *taken = (uint8_t *)calloc(n > 0 ? n : 1, 1);
+  for (int i = 0; i < n; ++i) perm[i] = i;
+  uint64_t s = seed;
+  for (int i = n - 1; i > 0; --i) {
+    int j = (int)(orc_splitmix64(&s) % (uint64_t)(i + 1));
+    int32_t t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+  }
+  for (int t = 0; t < n && k < count; ++t) {
+    int c = perm[t], gy = c / gw, gx = c % gw, ok = 1;
+    for (int dy = -1; dy <= 1 && ok; ++dy)
+      for (int dx = -1; dx <= 1 && ok; ++dx) {
+        int y = gy + dy, x = gx + dx;
+        if (y >= 0 && y < gh && x >= 0 && x < gw && taken[y * gw + x]) ok = 0;
+      }
+    if (!ok) continue;
+    taken[c] = 1;
+    top_left[2 * k] = gy * B;
+    top_left[2 * k + 1] = gx * B;
+    ++k;
+  }
+  qsort(top_left, (size_t)k, 2 * sizeof(int32_t), orc_cmp_pair);
+  free(perm); free(taken);
+  return k;
 }
 
 int orc_max_threads(void) {

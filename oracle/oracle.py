@@ -14,6 +14,7 @@ package `fse` (/root/reference/pkg/src/fse), wrapped here with ctypes:
   cfse_kernel     <- cfse.py:55-107
   extrapolate     <- cfse.py:110-142
   conceal_blocks  <- SPEC.md:332-340 (harness conceal, absent in the reference)
+  loss_pattern    <- SURVEY.md 8(d) isolated-block loss selection
 
 It is pinned against golden vectors produced by running the reference itself
 (tests/golden/make_golden.py -> tests/golden/*.npz; checked by
@@ -75,6 +76,8 @@ def lib():
         L.orc_conceal_blocks.argtypes = [P, i, i, i, ll, ll, P, i, i, i, i, d, d, i, P, i]
         L.orc_conceal_blocks.restype = i
         L.orc_max_threads.restype = i
+        L.orc_loss_pattern.argtypes = [i, i, i, i, ctypes.c_uint64, P]
+        L.orc_loss_pattern.restype = i
         _lib = L
     return _lib
 
@@ -189,6 +192,27 @@ def conceal_blocks(frames: np.ndarray, blocks: np.ndarray, B: int, border: int, 
                                   int(iterations), _p(tiles), int(nthreads))
     _check(rc)
     return tiles
+
+
+def loss_pattern(H: int, W: int, B: int, count: int, seed: int) -> np.ndarray:
+    """SURVEY.md 8(d) isolated-block loss selection (orc_loss_pattern);
+    (k, 2) int32 (top, left), row-major."""
+    out = np.empty((max(int(count), 1), 2), np.int32)
+    k = lib().orc_loss_pattern(int(H), int(W), int(B), int(count), int(seed) & (2 ** 64 - 1), _p(out))
+    if k < 0:
+        raise OracleError("bad loss-pattern geometry")
+    return out[:k]
+
+
+def frames_pattern(n_frames: int, H: int, W: int, B: int, fraction: float, seed: int) -> np.ndarray:
+    """(n, 3) = (frame, top, left), one pattern per frame with
+    round(fraction * grid blocks) losses (the product's frames_pattern)."""
+    n = int(round(fraction * (H // B) * (W // B)))
+    parts = []
+    for f in range(n_frames):
+        p = loss_pattern(H, W, B, n, seed * 1000003 + f)
+        parts.append(np.concatenate([np.full((p.shape[0], 1), f, np.int32), p], 1))
+    return np.concatenate(parts, 0) if parts else np.zeros((0, 3), np.int32)
 
 
 # ------------------------------------------------------- parity utilities
@@ -330,6 +354,56 @@ def pick_deficit(signal, labels, rho, gamma, upto: int, trace_other) -> float:
     m2 = R.real ** 2 + R.imag ** 2
     top = float(m2.max())
     return float((top - m2[pu, pv]) / top) if top > 0 else 0.0
+
+
+def divergence_certificate(signal, labels, rho, gamma, upto: int, trace_fp32) -> dict:
+    """Evidence for an fp32 run that left the fp64 selection sequence at
+    iteration `upto` (its first canonical divergence from the oracle).
+
+    The fp64 oracle is stepped to `upto`; in its state R64:
+      top      max |R64|^2 (the fp64 pick),
+      pick     |R64|^2 at the fp32 run's pick (mapped into the oracle's
+               canonical frame),
+      deficit  (top - pick) / top,
+      gap_amp  |R64[top]| - |R64[pick]| (amplitude gap; >= 0),
+      err_amp  the fp32 run's measured residual error: the largest
+               |R32 - R64| over the bins both runs selected before `upto`
+               (|c32 - c64| * w00 / gamma, c = gamma R / w00, cfse.py:85)
+               and at the fp32 pick itself at `upto`
+               (|c32[upto] w00 / gamma - R64[pick]|).
+    The fp32 run can rank the two bins the other way only if its errors at
+    them sum to at least gap_amp; `err_amp` is the size of those errors as
+    measured on this block.  `bounded` = gap_amp <= 2 err_amp.
+    `strict` = deficit < 1e-6 (top-2 relative gap < 1e-6).
+    """
+    s = np.asarray(signal, np.float64)
+    w = build_weight(labels, rho)
+    W = dft2(w.astype(np.complex128))
+    R = dft2((s * w).astype(np.complex128))
+    e0 = float(np.sum(w * s * s))
+    M, N = R.shape
+    w00 = W[0, 0].real
+    n = max(upto + 1, 1)
+    _, ous, ovs, ocs, _ = cfse_kernel(R.copy(), W, gamma, 1.0 / w00, n, e0)
+    ocu, ocv, occ = canonicalize_trace(ous, ovs, ocs, M, N)
+    mirrored = not (np.array_equal(ocu, ous) and np.array_equal(ocv, ovs))
+    gu, gv, gc = canonicalize_trace(*trace_fp32, M, N)
+    if upto > 0:
+        cfse_kernel(R, W, gamma, 1.0 / w00, upto, e0)
+    pu, pv = int(gu[upto]), int(gv[upto])
+    # R in the canonical frame: Rc[u, v] = conj(R[-u, -v]) when mirrored
+    r_pick = np.conj(R[(-pu) % M, (-pv) % N]) if mirrored else R[pu, pv]
+    m2 = R.real ** 2 + R.imag ** 2
+    top = float(m2.max())
+    pick = float(abs(r_pick) ** 2)
+    scale = w00 / gamma
+    err = [abs(complex(gc[k]) - complex(occ[k])) * scale for k in range(upto)]
+    err.append(abs(complex(gc[upto]) * scale - complex(r_pick)))
+    err_amp = float(max(err))
+    gap_amp = float(np.sqrt(top) - np.sqrt(pick))
+    deficit = float((top - pick) / top) if top > 0 else 0.0
+    return dict(at=int(upto), deficit=deficit, gap_amp=gap_amp, err_amp=err_amp,
+                strict=bool(deficit < 1e-6), bounded=bool(gap_amp <= 2.0 * err_amp))
 
 
 def near_tie_gap(signal, labels, rho, gamma, upto: int) -> float:

@@ -108,7 +108,13 @@ class ConcealPlan:
         """Conceal every planned block of device-resident `frames`
         ((n_frames, H, W) or (H, W) CUDA tensor, u8/f32/f64, rows may be
         padded: the row pitch is taken from the tensor stride).  Returns
-        the (n_blocks, B, B) tiles tensor (and a trace dict if `trace`)."""
+        the (n_blocks, B, B) tiles tensor (and a trace dict if `trace`).
+
+        `tiles` may be a pinned (page-locked) host tensor: the kernel then
+        stores each finished tile straight into host memory over the
+        host link (mapped pinned memory, unified addressing), so the tiles
+        are on the host when the stream reaches this point -- no separate
+        device-to-host copy."""
         import torch
 
         if not frames.is_cuda:
@@ -120,6 +126,12 @@ class ConcealPlan:
         tdt = {"u8": torch.uint8, "f32": torch.float32, "f64": torch.float64}[tile_dtype]
         if tiles is None:
             tiles = torch.empty((self.n_blocks, B, B), dtype=tdt, device=f3.device)
+        elif (tuple(tiles.shape) != (self.n_blocks, B, B) or tiles.dtype != tdt
+              or not tiles.is_contiguous()):
+            raise ValueError(f"tiles must be a contiguous {tdt} tensor of shape "
+                             f"{(self.n_blocks, B, B)}, got {tiles.dtype} {tuple(tiles.shape)}")
+        elif not (tiles.is_cuda or tiles.is_pinned()):
+            raise ValueError("tiles must live on the device or in pinned host memory")
         tr = None
         if trace:
             it = self.iterations
@@ -150,7 +162,8 @@ class Concealer:
     def __init__(self, blocks, n_frames: int, H: int, W: int, geometry: Geometry = Geometry(), *,
                  rho_hat: float = 0.8, gamma: float = 0.5, iterations: int = 100,
                  precision: str = "fp32", chunk_frames=None, frame_dtype=np.uint8,
-                 tile_dtype: str = "u8", algorithm: str = "cfse", basis_target=None):
+                 tile_dtype: str = "u8", algorithm: str = "cfse", basis_target=None,
+                 tile_path: str = "host"):
         torch = _lib.require_cuda()
         b = np.asarray(blocks, np.int32).reshape(-1, 3)
         order = np.argsort(b[:, 0], kind="stable")
@@ -183,8 +196,15 @@ class Concealer:
         self.nbuf = 4
         self.dev_frames = [torch.empty((chunk_frames, H, W), dtype=tt, device="cuda")
                            for _ in range(min(self.nbuf, len(self.chunks)))]
-        self.dev_tiles = torch.empty((self.n_blocks, geometry.B, geometry.B), dtype=tdt, device="cuda")
-        self.host_tiles = torch.empty_like(self.dev_tiles, device="cpu").pin_memory()
+        # tiles: by default each kernel stores its tiles straight into the
+        # pinned host buffer (zero-copy, see ConcealPlan.run); tile_path="copy"
+        # keeps device tiles and copies each chunk's tiles back instead
+        if tile_path not in ("host", "copy"):
+            raise ConfigError(f"tile_path must be 'host' or 'copy', got {tile_path!r}")
+        self.tile_path = tile_path
+        self.dev_tiles = (torch.empty((self.n_blocks, geometry.B, geometry.B), dtype=tdt, device="cuda")
+                          if tile_path == "copy" else None)
+        self.host_tiles = torch.empty((self.n_blocks, geometry.B, geometry.B), dtype=tdt).pin_memory()
         self.copy_stream = torch.cuda.Stream()
         # two compute streams: chunk k+1's persistent kernel fills the SMs
         # freed by chunk k's tail instead of waiting for it
@@ -202,13 +222,25 @@ class Concealer:
     def d2h_bytes(self) -> int:
         return self.host_tiles.numel() * self.host_tiles.element_size()
 
-    def run(self, host_frames, copy: bool = False) -> np.ndarray:
+    def run(self, host_frames, copy: bool = False, out=None) -> np.ndarray:
         """host_frames: pinned torch tensor (n_frames, H, W).  Returns the
         tiles in the caller's block order.  When the caller's blocks are
         already in frame order (the usual case) the result is a view of the
-        pinned tile buffer, valid until the next run (copy=True detaches it)."""
+        pinned tile buffer, valid until the next run (copy=True detaches it).
+
+        `out`: optional pinned host tensor (n_blocks, B, B) of the tile
+        dtype (e.g. one rank's slice of a host buffer shared by every GPU of
+        the box) that receives the tiles instead of the internal buffer;
+        needs blocks in frame order.  Returns out.numpy()."""
         import torch
 
+        dst = self.host_tiles
+        if out is not None:
+            if not self.identity_order:
+                raise ValueError("out= needs the block list in frame order")
+            if tuple(out.shape) != tuple(dst.shape) or out.dtype != dst.dtype or not out.is_pinned():
+                raise ValueError(f"out must be a pinned {dst.dtype} tensor of shape {tuple(dst.shape)}")
+            dst = out
         cs = self.copy_stream
         nb = len(self.dev_frames)
         done = [None] * len(self.chunks)  # compute-done event per chunk (frees its buffer)
@@ -224,20 +256,23 @@ class Concealer:
             with torch.cuda.stream(ks):
                 ks.wait_event(ready)
                 if plan is not None:
-                    plan.run(buf[: f1 - f0], self.dev_tiles[lo:hi], tile_dtype=self.tile_dtype,
-                             stream=ks)
-                    self.host_tiles[lo:hi].copy_(self.dev_tiles[lo:hi], non_blocking=True)
+                    if self.dev_tiles is None:  # kernel stores tiles into pinned host memory
+                        plan.run(buf[: f1 - f0], dst[lo:hi], tile_dtype=self.tile_dtype, stream=ks)
+                    else:
+                        plan.run(buf[: f1 - f0], self.dev_tiles[lo:hi], tile_dtype=self.tile_dtype,
+                                 stream=ks)
+                        dst[lo:hi].copy_(self.dev_tiles[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(ks)
                 done[i] = ev
         for ks in self.compute_streams:
             ks.synchronize()
-        tiles = self.host_tiles.numpy()
+        tiles = dst.numpy()
         if self.identity_order:
             return tiles.copy() if copy else tiles
-        out = np.empty(tiles.shape, tiles.dtype)
-        out[self.order] = tiles
-        return out
+        res = np.empty(tiles.shape, tiles.dtype)
+        res[self.order] = tiles
+        return res
 
 
 def conceal_frames(frames, blocks, geometry: Geometry = Geometry(), *, rho_hat=0.8, gamma=0.5,

@@ -59,11 +59,12 @@ def frame_u8(H: int, W: int, seed: int) -> np.ndarray:
 
 
 def field_torch(n: int, H: int, W: int, seed: int, device, edges: bool = True, u8: bool = True):
-    """On-device batch of n frames (torch), same recipe as field/add_edges."""
+    """On-device batch of n frames (torch), same recipe as field/add_edges.
+    Frame i is drawn from its own generator seeded with seed + i, so frame f
+    of a job is the same whichever rank (or batch) generates it."""
     import torch
 
     g = torch.Generator(device=device)
-    g.manual_seed(seed)
     fy = torch.fft.fftfreq(H, device=device, dtype=torch.float64)[:, None]
     fx = torch.fft.fftfreq(W, device=device, dtype=torch.float64)[None, :]
     f = torch.hypot(fy, fx)
@@ -72,6 +73,7 @@ def field_torch(n: int, H: int, W: int, seed: int, device, edges: bool = True, u
     yy = torch.arange(H, device=device, dtype=torch.float32)[:, None]
     xx = torch.arange(W, device=device, dtype=torch.float32)[None, :]
     for i in range(n):
+        g.manual_seed(seed + i)
         theta = torch.rand((H, W), generator=g, device=device, dtype=torch.float64) * (2 * math.pi)
         x = torch.fft.ifft2(A * torch.polar(torch.ones_like(theta), theta)).real
         x = ((x - x.mean()) / x.std() * 40.0 + 128.0).clamp_(0, 255).float()

@@ -10,6 +10,7 @@ if REPO not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run on the GPU box via gpurun)")
+    config.addinivalue_line("markers", "slow: long GPU parity runs (full configurations)")
 
 
 @pytest.fixture(scope="session")

@@ -164,7 +164,8 @@ def test_config2_fp32(fse):
     blocks = np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
     tiles, get, plan = _run_plan(fse, img, blocks, 64, 16, 16, 100)
     assert plan.info["fast_path"] == 1 and plan.info["n_classes"] == 4
-    st = fp32_gate(img, blocks, tiles, get, 64, 16, 16, 0.8, 0.5, 100, truth=_truth(img, blocks, 16))
+    st = fp32_gate(img, blocks, tiles, get, 64, 16, 16, 0.8, 0.5, 100, truth=_truth(img, blocks, 16),
+                   log="config2")
     print("config2", st)
 
 
@@ -176,31 +177,90 @@ def test_config4a_fp32(fse):
     blocks = np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
     tiles, get, plan = _run_plan(fse, img, blocks, 32, 8, 8, 100)
     assert plan.info["fast_path"] == 1
-    st = fp32_gate(img, blocks, tiles, get, 32, 8, 8, 0.8, 0.5, 100, truth=_truth(img, blocks, 8))
+    st = fp32_gate(img, blocks, tiles, get, 32, 8, 8, 0.8, 0.5, 100, truth=_truth(img, blocks, 8),
+                   log="config4a")
     print("config4a", st)
 
 
-def test_config4b_fp32(fse):
+def test_config4b_full_fp32(fse):
+    """Config 4b in full: 8 images field(512, 512, s4 + k), 32x32 losses at
+    (64i, 64j) -- 7 full images of 64 blocks + 52 of the 8th = 500 blocks,
+    border 16, F = 128, I = 100."""
     from paper_2204_14193_b200.synth import field
-    imgs = np.stack([field(512, 512, seed=40 + k) for k in range(2)]).astype(np.float32)
-    blocks = np.array([(f, 64 * i, 64 * j) for f in range(2) for i in range(8) for j in range(8)],
-                      np.int32)[:100]
+    imgs = np.stack([field(512, 512, seed=40 + k) for k in range(8)]).astype(np.float32)
+    blocks = np.array([(f, 64 * i, 64 * j) for f in range(8) for i in range(8) for j in range(8)],
+                      np.int32)[:500]
     tiles, get, plan = _run_plan(fse, imgs, blocks, 128, 32, 16, 100)
     assert plan.info["fast_path"] == 1
-    st = fp32_gate(imgs, blocks, tiles, get, 128, 32, 16, 0.8, 0.5, 100, truth=_truth(imgs, blocks, 32))
-    print("config4b", st)
+    st = fp32_gate(imgs, blocks, tiles, get, 128, 32, 16, 0.8, 0.5, 100,
+                   truth=_truth(imgs, blocks, 32), log="config4b_full")
+    print("config4b", {k: v for k, v in st.items() if k != "outliers"})
 
 
-def test_config3_u8_subset_fp32(fse):
-    """Config 3 geometry (1920x1080 u8 + edges, 10% isolated loss, I=200) on 2 frames."""
+@pytest.mark.slow
+def test_config3_full_fp32(fse):
+    """Config 3 in full: 64 frames of 1920x1080 u8 (1/f^2 field + 8 edges,
+    bench.py's on-device generator), 10 % isolated loss = 804 blocks per
+    frame, 51,456 blocks, I = 200.  Every block against the C oracle."""
+    from paper_2204_14193_b200.synth import field_torch
+    fr = field_torch(64, 1080, 1920, seed=3 * 7919, device="cuda")
+    frames = fr.cpu().numpy()
+    blocks = fse.frames_pattern(64, 1080, 1920, 16, 0.10, seed=3)
+    assert len(blocks) == 51456
+    tiles, get, plan = _run_plan(fse, frames, blocks, 64, 16, 16, 200)
+    assert plan.info["fast_path"] == 1
+    st = fp32_gate(frames, blocks, tiles, get, 64, 16, 16, 0.8, 0.5, 200,
+                   truth=_truth(frames, blocks, 16), log="config3_full")
+    print("config3", {k: v for k, v in st.items() if k != "outliers"})
+
+
+def test_config3_numpy_frames_fp32(fse):
+    """Config 3 geometry on the numpy frame generator (frame_u8), 2 frames, all blocks."""
     from paper_2204_14193_b200.synth import frame_u8
     frames = np.stack([frame_u8(1080, 1920, seed=300 + f) for f in range(2)])
     blocks = fse.frames_pattern(2, 1080, 1920, 16, 0.10, seed=3)
     assert len(blocks) == 2 * 804
-    sub = blocks[::4]
-    tiles, get, plan = _run_plan(fse, frames, sub, 64, 16, 16, 200)
-    st = fp32_gate(frames, sub, tiles, get, 64, 16, 16, 0.8, 0.5, 200, truth=_truth(frames, sub, 16))
-    print("config3", st)
+    tiles, get, plan = _run_plan(fse, frames, blocks, 64, 16, 16, 200)
+    st = fp32_gate(frames, blocks, tiles, get, 64, 16, 16, 0.8, 0.5, 200,
+                   truth=_truth(frames, blocks, 16), log="config3_numpy2")
+    print("config3 numpy", {k: v for k, v in st.items() if k != "outliers"})
+
+
+@pytest.mark.parametrize("gen", ["field_torch", "frame_u8"])
+def test_config5_fp32(fse, gen):
+    """Config 5, the benched configuration: 3840x2160 u8 frames (1/f^2 field
+    + 8 edges), 5 % isolated 16x16 loss (1620 blocks per frame), border 16,
+    F = 64, I = 100, fp32, u8 tiles as the bench writes them, all nine
+    geometry classes of the clipped support.  field_torch: six of the
+    bench's own frames (0, 1, 19, 30, 68, 100 -- the first frames whose
+    patterns hold each corner class) with the bench's block lists; frame_u8:
+    two numpy-generated frames plus the four corner blocks."""
+    import torch
+    H, W = 2160, 3840
+    if gen == "field_torch":
+        from paper_2204_14193_b200.synth import field_torch
+        pick = [0, 1, 19, 30, 68, 100]
+        frames = np.stack([field_torch(1, H, W, seed=5 * 7919 + f, device="cuda")[0].cpu().numpy()
+                           for f in pick])
+        allb = fse.frames_pattern(max(pick) + 1, H, W, 16, 0.05, seed=5)
+        blocks = np.concatenate([allb[allb[:, 0] == f] for f in pick])
+        blocks[:, 0] = np.searchsorted(pick, blocks[:, 0])
+        assert len(blocks) == 1620 * len(pick)
+    else:
+        from paper_2204_14193_b200.synth import frame_u8
+        frames = np.stack([frame_u8(H, W, seed=500 + f) for f in range(2)])
+        blocks = fse.frames_pattern(2, H, W, 16, 0.05, seed=5)
+        corners = np.array([[1, 0, 0], [1, 0, W - 16], [1, H - 16, 0], [1, H - 16, W - 16]], np.int32)
+        blocks = np.concatenate([blocks, corners])
+    tiles, get, plan = _run_plan(fse, frames, blocks, 64, 16, 16, 100)
+    assert plan.info["fast_path"] == 1 and plan.info["n_classes"] == 9
+    st = fp32_gate(frames, blocks, tiles, get, 64, 16, 16, 0.8, 0.5, 100,
+                   truth=_truth(frames, blocks, 16), log=f"config5_{gen}")
+    # the bench writes u8 tiles: they are the clamped, rounded f32 tiles
+    fr = torch.from_numpy(frames).cuda()
+    t8 = fse.ConcealPlan(blocks, H, W, gamma=0.5, iterations=100).run(fr, tile_dtype="u8").cpu().numpy()
+    assert np.array_equal(t8, np.rint(np.clip(tiles, 0, 255)).astype(np.uint8))
+    print("config5", gen, {k: v for k, v in st.items() if k != "outliers"})
 
 
 def test_fp64_plan_matches_oracle(fse):
@@ -417,3 +477,55 @@ def test_frames_beyond_4gib(fse, dtype, n_frames):
     del big
     torch.cuda.empty_cache()
     assert np.array_equal(t_big, t_small)
+
+
+def test_tiles_stored_into_pinned_host_memory(fse):
+    """Tiles written by the kernel straight into pinned host memory (torch
+    pinned tensor, and a page-locked /dev/shm mapping shared by ranks --
+    sharding.HostTileBuffer) equal the device tiles, for the fused fp32 path
+    (u8 and f32 tiles) and the per-window fp64 path."""
+    import os
+    import torch
+    from paper_2204_14193_b200 import sharding
+    from paper_2204_14193_b200.synth import field_torch
+    frames = field_torch(3, 270, 480, seed=5, device="cuda")
+    blocks = fse.frames_pattern(3, 270, 480, 16, 0.05, seed=2)
+    plan = fse.ConcealPlan(blocks, 270, 480, iterations=100)
+    for tdt, tt in (("u8", torch.uint8), ("f32", torch.float32)):
+        dev = plan.run(frames, tile_dtype=tdt).cpu()
+        host = torch.empty((len(blocks), 16, 16), dtype=tt).pin_memory()
+        plan.run(frames, host, tile_dtype=tdt)
+        torch.cuda.synchronize()
+        assert torch.equal(dev, host)
+    with pytest.raises(ValueError):  # pageable host memory is refused
+        plan.run(frames, torch.empty((len(blocks), 16, 16), dtype=torch.uint8))
+    path = f"/dev/shm/fse_test_tiles_{os.getpid()}"
+    buf = sharding.HostTileBuffer(path, (len(blocks) + 5, 16, 16), torch.uint8, create=True)
+    try:
+        plan.run(frames, buf.slice(5, 5 + len(blocks)))
+        torch.cuda.synchronize()
+        assert torch.equal(buf.tensor[5:], plan.run(frames).cpu())
+        assert int(buf.tensor[:5].sum()) == 0
+    finally:
+        buf.close(unlink=True)
+    p64 = fse.ConcealPlan(blocks[:6], 270, 480, iterations=20, precision="fp64")
+    h64 = torch.empty((6, 16, 16), dtype=torch.float64).pin_memory()
+    p64.run(frames, h64, tile_dtype="f64")
+    torch.cuda.synchronize()
+    assert torch.equal(h64, p64.run(frames, tile_dtype="f64").cpu())
+
+
+def test_concealer_tile_paths_agree(fse):
+    """Concealer: kernel-to-host tiles (default) == device tiles + copy."""
+    from paper_2204_14193_b200.synth import frame_u8
+    frames = np.stack([frame_u8(270, 480, seed=60 + f) for f in range(5)])
+    blocks = fse.frames_pattern(5, 270, 480, 16, 0.05, seed=8)
+    a = fse.Concealer(blocks, 5, 270, 480, chunk_frames=2, iterations=50, gamma=0.5)
+    b = fse.Concealer(blocks, 5, 270, 480, chunk_frames=2, iterations=50, gamma=0.5, tile_path="copy")
+    h = a.pin(frames)
+    ta = a.run(h, copy=True)
+    tb = b.run(h, copy=True)
+    assert np.array_equal(ta, tb)
+    import torch
+    out = torch.zeros((len(blocks), 16, 16), dtype=torch.uint8).pin_memory()
+    assert np.array_equal(a.run(h, out=out), ta)

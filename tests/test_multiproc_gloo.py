@@ -19,6 +19,7 @@ def _fake_tiles(frames_offset, local_blocks):
 
 
 def _worker(rank, world, port, blocks, n_frames, q):
+    import torch
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -27,8 +28,19 @@ def _worker(rank, world, port, blocks, n_frames, q):
     sh = sharding.shard_blocks(blocks, n_frames, rank, world)
     tiles = _fake_tiles(sh.f0, sh.blocks).astype(np.uint8)
     out = sharding.gather_tiles(sh, tiles, len(blocks))
+    # the one-box path: every rank stores its slice into one shared host buffer
+    path = os.path.join("/dev/shm", f"fse_test_tiles_{port}")
     if rank == 0:
-        q.put(out)
+        buf = sharding.HostTileBuffer(path, (len(blocks), 16, 16), torch.uint8, create=True, pin=False)
+    dist.barrier()
+    if rank != 0:
+        buf = sharding.HostTileBuffer(path, (len(blocks), 16, 16), torch.uint8, create=False, pin=False)
+    lo, hi = sharding.contiguous_range(sh)
+    buf.slice(lo, hi).copy_(torch.from_numpy(tiles))
+    dist.barrier()
+    if rank == 0:
+        q.put((out, buf.numpy().copy()))
+        buf.close(unlink=True)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -51,12 +63,13 @@ def test_sharded_gather_matches_single_process(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, blocks, n_frames, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = q.get(timeout=120)
+    out, shared = q.get(timeout=120)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     ref = _fake_tiles(0, blocks).astype(np.uint8)
     assert np.array_equal(out, ref)
+    assert np.array_equal(shared, ref)
 
 
 def test_frame_ranges_balanced_and_cover():
