@@ -178,8 +178,10 @@ int fse_plan_get_info(const fse_plan *plan, fse_plan_info *info);
 int fse_plan_destroy(fse_plan *plan);
 
 /* Run a plan.  frames: device, dtype FSE_U8/F32/F64, frame f row y starts
- * at frames + f*frame_stride + y*pitch (elements).  tiles: device,
- * n_blocks x B x B of tile_dtype (FSE_U8: clamp [0,255] + round-half-even;
+ * at frames + f*frame_stride + y*pitch (elements).  tiles: device memory or
+ * page-locked host memory (unified addressing: the kernel stores each tile
+ * straight into host memory), n_blocks x B x B of tile_dtype (FSE_U8:
+ * clamp [0,255] + round-half-even;
  * FSE_F32 / FSE_F64: unclamped Re{g}).  trace_uv (int32 n x I x 2),
  * trace_c (float32/64 n x I x 2 per precision), trace_e (float32/64 n x I):
  * optional (NULL).  Asynchronous on `stream`. */

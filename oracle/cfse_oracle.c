@@ -17,6 +17,9 @@
  *   orc_extrapolate     <- cfse.py:28-52,110-142 (_prepare + extrapolate_cfse)
  *   orc_conceal_blocks  <- SPEC.md:332-340       (harness `conceal`: centred
  *                          F x F window, valid_rect = image, write Re{g})
+ *   orc_rfse_kernel     <- rfse.py:37-167        (_pair_tables + _rfse_kernel)
+ *   orc_extrapolate_rfse<- rfse.py:170-210       (extrapolate_rfse)
+ *   orc_conceal_blocks_rfse                      (conceal with rFSE)
  *   orc_loss_pattern    <- SURVEY.md 8(d)        (seeded isolated-block loss
  *                          selection; the bench's reference-arm block list)
  *
@@ -320,6 +323,222 @@ int orc_conceal_blocks(const void *frames, int dtype, int H, int Wd,
           tiles[(size_t)b * B * B + (size_t)i * B + j] = rec[(size_t)(off + i) * F + off + j];
     }
     free(s); free(rec); free(lab); free(us); free(vs); free(cs); free(es);
+  }
+  return err;
+}
+
+/* ------------------------------------------------------------ rFSE */
+
+/* rfse.py:37-55 (_pair_tables) + 56-167 (_rfse_kernel), numba order.
+ * R (c128 M x N) mutated in place; W the weight spectrum; w00 = W[0,0].re.
+ * Runs until `max_iters` iterations or the basis-function tally reaches
+ * `stop_tally`.  Trace arrays hold max_iters entries; returns the count
+ * executed (*tally = basis functions), or -7 when the pair Gram
+ * determinant is degenerate (ConfigError, rfse.py:50-54).  G nullable. */
+int orc_rfse_kernel(int M, int N, double *R, const double *W, double gamma,
+                    double w00, int max_iters, int stop_tally, double e0,
+                    double *G, int64_t *us, int64_t *vs, double *cs,
+                    double *es, uint8_t *selfs, int *tally_out) {
+  size_t mn = (size_t)M * N;
+  double dmn = (double)mn;
+  double *W2 = (double *)malloc(sizeof(double) * 2 * mn);
+  double *D = (double *)malloc(sizeof(double) * mn);
+  uint8_t *sc = (uint8_t *)malloc(mn);
+  for (int k = 0; k < M; ++k)
+    for (int l = 0; l < N; ++l) {
+      size_t i = (size_t)k * N + l;
+      int k2 = (2 * k) % M, l2 = (2 * l) % N;
+      const double *w2 = W + 2 * ((size_t)k2 * N + l2);
+      W2[2 * i] = w2[0]; W2[2 * i + 1] = w2[1];
+      sc[i] = (k2 == 0 && l2 == 0);
+      D[i] = w00 * w00 - (w2[0] * w2[0] + w2[1] * w2[1]);
+      if (!sc[i] && D[i] <= 1e-9 * w00 * w00) {
+        free(W2); free(D); free(sc);
+        return -7;
+      }
+    }
+  if (G) memset(G, 0, sizeof(double) * 2 * mn);
+  double damp = gamma * (2.0 - gamma), e = e0;
+  int count = 0, tally = 0;
+  while (count < max_iters && tally < stop_tally) {
+    double best = -1.0, bpr = 0.0, bpi = 0.0;
+    int bu = 0, bv = 0, bself = 1;
+    for (int k = 0; k < M; ++k)
+      for (int l = 0; l < N; ++l) {
+        size_t i = (size_t)k * N + l;
+        double ar = R[2 * i], ai = R[2 * i + 1];
+        if (sc[i]) {
+          double pr = ar / w00, crit = ar * pr;
+          if (crit > best) { best = crit; bu = k; bv = l; bpr = pr; bpi = 0.0; bself = 1; }
+        } else {
+          double w2r = W2[2 * i], w2i = W2[2 * i + 1];
+          double nr = w00 * ar - (w2r * ar + w2i * ai);
+          double ni = w00 * ai - (w2i * ar - w2r * ai);
+          double d = D[i];
+          double pr = nr / d, pi = ni / d;
+          double crit = 2.0 * (pr * ar + pi * ai);
+          if (crit > best) { best = crit; bu = k; bv = l; bpr = pr; bpi = pi; bself = 0; }
+        }
+      }
+    int u = bu, v = bv;
+    if (!bself) {
+      int mu = (M - u) % M, mv = (N - v) % N;
+      if (mu * N + mv < u * N + v) { u = mu; v = mv; bpi = -bpi; }
+    }
+    /* c = gamma * complex(bpr, bpi) */
+    double cr = gamma * bpr - 0.0 * bpi, ci = gamma * bpi + 0.0 * bpr;
+    if (G) {
+      G[2 * ((size_t)u * N + v)] += dmn * cr - 0.0 * ci;
+      G[2 * ((size_t)u * N + v) + 1] += dmn * ci + 0.0 * cr;
+    }
+    if (bself) {
+      for (int k = 0; k < M; ++k) {
+        int ks = k - u;
+        if (ks < 0) ks += M;
+        for (int l = 0; l < N; ++l) {
+          int ls = l - v;
+          if (ls < 0) ls += N;
+          const double *w = W + 2 * ((size_t)ks * N + ls);
+          double *x = R + 2 * ((size_t)k * N + l);
+          x[0] = x[0] - (cr * w[0] - ci * w[1]);
+          x[1] = x[1] - (cr * w[1] + ci * w[0]);
+        }
+      }
+      tally += 1;
+    } else {
+      int mu = (M - u) % M, mv = (N - v) % N;
+      double ccr = cr, cci = -ci;
+      if (G) {
+        G[2 * ((size_t)mu * N + mv)] += dmn * ccr - 0.0 * cci;
+        G[2 * ((size_t)mu * N + mv) + 1] += dmn * cci + 0.0 * ccr;
+      }
+      for (int k = 0; k < M; ++k) {
+        int ks = k - u, ks2 = k - mu;
+        if (ks < 0) ks += M;
+        if (ks2 < 0) ks2 += M;
+        for (int l = 0; l < N; ++l) {
+          int ls = l - v, ls2 = l - mv;
+          if (ls < 0) ls += N;
+          if (ls2 < 0) ls2 += N;
+          const double *w = W + 2 * ((size_t)ks * N + ls);
+          const double *w2 = W + 2 * ((size_t)ks2 * N + ls2);
+          double *x = R + 2 * ((size_t)k * N + l);
+          /* (R - c W) - conj(c) W' */
+          double t0 = x[0] - (cr * w[0] - ci * w[1]);
+          double t1 = x[1] - (cr * w[1] + ci * w[0]);
+          x[0] = t0 - (ccr * w2[0] - cci * w2[1]);
+          x[1] = t1 - (ccr * w2[1] + cci * w2[0]);
+        }
+      }
+      tally += 2;
+    }
+    e -= damp * best;
+    us[count] = u; vs[count] = v;
+    cs[2 * count] = cr; cs[2 * count + 1] = ci;
+    es[count] = e;
+    selfs[count] = (uint8_t)bself;
+    ++count;
+  }
+  free(W2); free(D); free(sc);
+  if (tally_out) *tally_out = tally;
+  return count;
+}
+
+/* rfse.py:170-210 (extrapolate_rfse): _prepare, pair tables, loop, Re{idft2}
+ * on the loss.  basis_target < 0: fixed count `iters`; else max_iters =
+ * stop_tally = basis_target.  Returns the iteration count (>= 0) or a
+ * negative error (-6 empty support, -7 degenerate pairs). */
+int orc_extrapolate_rfse(int M, int N, const double *s, const int8_t *labels,
+                         double rho, double gamma, int iters, int basis_target,
+                         double *recon, int64_t *us, int64_t *vs, double *cs,
+                         double *es, uint8_t *selfs, int *tally) {
+  size_t mn = (size_t)M * N;
+  double *w = (double *)malloc(sizeof(double) * mn);
+  double *W = (double *)malloc(sizeof(double) * 2 * mn);
+  double *R = (double *)malloc(sizeof(double) * 2 * mn);
+  double *G = (double *)malloc(sizeof(double) * 2 * mn);
+  orc_build_weight(M, N, labels, rho, w);
+  for (size_t i = 0; i < mn; ++i) { W[2 * i] = w[i]; W[2 * i + 1] = 0.0; }
+  orc_dft2(M, N, W, W, 0);
+  double w00 = W[0];
+  int rc;
+  if (w00 <= 1e-12 * (double)M * (double)N) {
+    rc = -6;
+  } else {
+    double e0 = 0.0;
+    for (size_t i = 0; i < mn; ++i) {
+      R[2 * i] = s[i] * w[i]; R[2 * i + 1] = 0.0;
+      e0 += w[i] * s[i] * s[i];
+    }
+    orc_dft2(M, N, R, R, 0);
+    int max_it = basis_target >= 0 ? basis_target : iters;
+    int stop = basis_target >= 0 ? basis_target : 2 * iters + 1;
+    rc = orc_rfse_kernel(M, N, R, W, gamma, w00, max_it, stop, e0, G, us, vs, cs, es, selfs, tally);
+    if (rc >= 0) {
+      orc_dft2(M, N, G, G, 1);
+      for (size_t i = 0; i < mn; ++i) recon[i] = labels[i] == AREA_LOSS ? G[2 * i] : s[i];
+    }
+  }
+  free(w); free(W); free(R); free(G);
+  return rc;
+}
+
+/* rFSE per-block concealment (as orc_conceal_blocks). */
+int orc_conceal_blocks_rfse(const void *frames, int dtype, int H, int Wd,
+                            long long pitch, long long frame_stride,
+                            const int32_t *blocks, int nblocks, int B, int border,
+                            int F, double rho, double gamma, int iters, int basis_target,
+                            double *tiles, int nthreads) {
+  int off = (F - B) / 2;
+  int err = 0;
+  int cap = basis_target >= 0 ? basis_target : iters;
+  if (cap < 1) cap = 1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+#endif
+  {
+    size_t mn = (size_t)F * F;
+    double *s = (double *)malloc(sizeof(double) * mn);
+    double *rec = (double *)malloc(sizeof(double) * mn);
+    int8_t *lab = (int8_t *)malloc(mn);
+    int64_t *us = (int64_t *)malloc(sizeof(int64_t) * cap);
+    int64_t *vs = (int64_t *)malloc(sizeof(int64_t) * cap);
+    double *cs = (double *)malloc(sizeof(double) * 2 * cap);
+    double *es = (double *)malloc(sizeof(double) * cap);
+    uint8_t *sf = (uint8_t *)malloc(cap);
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+    for (int b = 0; b < nblocks; ++b) {
+      int f = blocks[3 * b], top = blocks[3 * b + 1], left = blocks[3 * b + 2];
+      int wt = top - off, wl = left - off, tally = 0;
+      int rc = orc_build_mask(F, F, off, off, B, B, border, 1, -wt, -wl, H, Wd, lab);
+      if (rc == 0) {
+        const size_t fbase = (size_t)f * (size_t)frame_stride;
+        for (int m = 0; m < F; ++m)
+          for (int n = 0; n < F; ++n) {
+            int y = wt + m, x = wl + n;
+            s[(size_t)m * F + n] = (y >= 0 && y < H && x >= 0 && x < Wd)
+                                       ? pix(frames, dtype, fbase + (size_t)y * pitch + x)
+                                       : 0.0;
+          }
+        rc = orc_extrapolate_rfse(F, F, s, lab, rho, gamma, iters, basis_target, rec, us, vs, cs,
+                                  es, sf, &tally);
+        if (rc > 0) rc = 0;
+      }
+      if (rc != 0) {
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+        { if (!err) err = rc; }
+        continue;
+      }
+      for (int i = 0; i < B; ++i)
+        for (int j = 0; j < B; ++j)
+          tiles[(size_t)b * B * B + (size_t)i * B + j] = rec[(size_t)(off + i) * F + off + j];
+    }
+    free(s); free(rec); free(lab); free(us); free(vs); free(cs); free(es); free(sf);
   }
   return err;
 }

@@ -74,6 +74,53 @@ def fp32_gate(frames, blocks, tiles_gpu, traces_gpu, F, B, border, rho, gamma, i
     return stats
 
 
+def first_rfse_divergence(trace_a, trace_b):
+    """First iteration whose (u, v) differ (rFSE traces carry the canonical
+    pair member already, rfse.py:113-121); None if identical."""
+    ua, va = np.asarray(trace_a[0]), np.asarray(trace_a[1])
+    ub, vb = np.asarray(trace_b[0]), np.asarray(trace_b[1])
+    n = min(len(ua), len(ub))
+    d = np.nonzero((ua[:n] != ub[:n]) | (va[:n] != vb[:n]))[0]
+    if d.size:
+        return int(d[0])
+    return None if len(ua) == len(ub) else n
+
+
+def rfse_gate(frames, blocks, tiles_gpu, traces_gpu, F, B, border, rho, gamma, iters,
+              basis_target=None, px_tol=0.5, log=None):
+    """fp32 rFSE gate against the fp64 rFSE oracle (oracle/cfse_oracle.c,
+    restating rfse.py:37-210): per block max |dpx| <= px_tol except
+    certified near-ties (oracle.rfse_divergence_certificate: strict =
+    criterion gap < 1e-6 relative at the first differing selection; bounded
+    = gap within twice the fp32 run's measured criterion error).  traces_gpu(k)
+    -> (us, vs, cs) of the fp32 run, trimmed to its executed iterations."""
+    fr = frames if frames.ndim == 3 else frames[None]
+    ref = orc.conceal_blocks_rfse(fr, blocks, B, border, F, rho, gamma, iters, basis_target)
+    g = np.asarray(tiles_gpu, np.float64)
+    dev = np.abs(g - ref).reshape(len(blocks), -1).max(axis=1)
+    outliers, failed = [], []
+    for k in np.nonzero(dev > px_tol)[0]:
+        f, t, l = blocks[k]
+        s, lab = window_of(fr[f].astype(np.float64), t, l, F, B, border)
+        o = orc.extrapolate_rfse(s, lab, rho, gamma, iters, basis_target)
+        tr = traces_gpu(k)
+        at = first_rfse_divergence((o["us"], o["vs"]), tr)
+        if at is None or at >= len(tr[0]):
+            failed.append((int(k), float(dev[k]), "no selection divergence"))
+            continue
+        cert = orc.rfse_divergence_certificate(s, lab, rho, gamma, at, tr)
+        outliers.append(dict(block=int(k), dev=float(dev[k]), **cert))
+        if not (cert["strict"] or cert["bounded"]):
+            failed.append((int(k), float(dev[k]), cert))
+    stats = dict(n=len(blocks), max_dev=float(dev.max()) if len(dev) else 0.0,
+                 over=int((dev > px_tol).sum()), strict=sum(r["strict"] for r in outliers),
+                 bounded=sum((not r["strict"]) and r["bounded"] for r in outliers), outliers=outliers)
+    if log:
+        log_stats(log, stats)
+    assert not failed, f"uncertified fp32 rFSE outliers: {failed}"
+    return stats
+
+
 def psnr_tiles(truth, tiles) -> float:
     """Pooled PSNR over loss pixels: 10 log10(255^2 / MSE)."""
     d = np.asarray(truth, np.float64) - np.asarray(tiles, np.float64)

@@ -43,6 +43,7 @@ _ERRORS = {
     -4: "loss rectangle extends outside the valid region",
     -5: "mask geometry leaves no support samples",
     -6: "total support weight is numerically zero (empty support)",
+    -7: "support area is degenerate for pairwise selection",
 }
 
 
@@ -78,6 +79,12 @@ def lib():
         L.orc_max_threads.restype = i
         L.orc_loss_pattern.argtypes = [i, i, i, i, ctypes.c_uint64, P]
         L.orc_loss_pattern.restype = i
+        L.orc_rfse_kernel.argtypes = [i, i, P, P, d, d, i, i, d, P, P, P, P, P, P, P]
+        L.orc_rfse_kernel.restype = i
+        L.orc_extrapolate_rfse.argtypes = [i, i, P, P, d, d, i, i, P, P, P, P, P, P, P]
+        L.orc_extrapolate_rfse.restype = i
+        L.orc_conceal_blocks_rfse.argtypes = [P, i, i, i, ll, ll, P, i, i, i, i, d, d, i, i, P, i]
+        L.orc_conceal_blocks_rfse.restype = i
         _lib = L
     return _lib
 
@@ -190,6 +197,63 @@ def conceal_blocks(frames: np.ndarray, blocks: np.ndarray, B: int, border: int, 
     rc = lib().orc_conceal_blocks(_p(fr), _DT[fr.dtype], H, W, W, H * W, _p(bl), bl.shape[0],
                                   int(B), int(border), int(F), float(rho), float(gamma),
                                   int(iterations), _p(tiles), int(nthreads))
+    _check(rc)
+    return tiles
+
+
+def rfse_kernel(R_w: np.ndarray, W: np.ndarray, gamma: float, w00: float, max_iters: int,
+                stop_tally: int, e0: float):
+    """rfse.py:37-167 (_pair_tables + _rfse_kernel).  R_w mutated in place.
+    Returns (G, us, vs, cs, es, selfs, tally)."""
+    assert R_w.dtype == np.complex128 and R_w.flags.c_contiguous
+    W = np.ascontiguousarray(W, np.complex128)
+    M, N = R_w.shape
+    n = max(int(max_iters), 1)
+    G = np.zeros((M, N), np.complex128)
+    us = np.zeros(n, np.int64); vs = np.zeros(n, np.int64)
+    cs = np.zeros(n, np.complex128); es = np.zeros(n); sf = np.zeros(n, np.uint8)
+    t = ctypes.c_int(0)
+    k = lib().orc_rfse_kernel(M, N, _p(R_w), _p(W), float(gamma), float(w00), int(max_iters),
+                              int(stop_tally), float(e0), _p(G), _p(us), _p(vs), _p(cs), _p(es), _p(sf),
+                              ctypes.byref(t))
+    if k < 0:
+        _check(k)
+    return G, us[:k], vs[:k], cs[:k], es[:k], sf[:k], int(t.value)
+
+
+def extrapolate_rfse(signal, labels, rho, gamma, iterations, basis_target=None):
+    """rfse.py:170-210.  Returns dict(reconstructed, us, vs, cs, es, selfs, tally)."""
+    s = np.ascontiguousarray(signal, np.float64)
+    labels = np.ascontiguousarray(labels, np.int8)
+    M, N = s.shape
+    bt = -1 if basis_target is None else int(basis_target)
+    n = max(int(iterations) if bt < 0 else bt, 1)
+    rec = np.empty((M, N))
+    us = np.zeros(n, np.int64); vs = np.zeros(n, np.int64)
+    cs = np.zeros(n, np.complex128); es = np.zeros(n); sf = np.zeros(n, np.uint8)
+    t = ctypes.c_int(0)
+    k = lib().orc_extrapolate_rfse(M, N, _p(s), _p(labels), float(rho), float(gamma), int(iterations), bt,
+                                   _p(rec), _p(us), _p(vs), _p(cs), _p(es), _p(sf), ctypes.byref(t))
+    if k < 0:
+        _check(k)
+    return dict(reconstructed=rec, us=us[:k], vs=vs[:k], cs=cs[:k], es=es[:k], selfs=sf[:k],
+                tally=int(t.value))
+
+
+def conceal_blocks_rfse(frames: np.ndarray, blocks: np.ndarray, B: int, border: int, F: int,
+                        rho: float, gamma: float, iterations: int, basis_target=None,
+                        nthreads: int = 0) -> np.ndarray:
+    """conceal_blocks with rFSE (rfse.py:170-210) per window."""
+    fr = np.ascontiguousarray(frames)
+    if fr.ndim == 2:
+        fr = fr[None]
+    nf, H, W = fr.shape
+    bl = np.ascontiguousarray(blocks, np.int32).reshape(-1, 3)
+    tiles = np.empty((bl.shape[0], B, B), np.float64)
+    rc = lib().orc_conceal_blocks_rfse(_p(fr), _DT[fr.dtype], H, W, W, H * W, _p(bl), bl.shape[0],
+                                       int(B), int(border), int(F), float(rho), float(gamma),
+                                       int(iterations), -1 if basis_target is None else int(basis_target),
+                                       _p(tiles), int(nthreads))
     _check(rc)
     return tiles
 
@@ -404,6 +468,111 @@ def divergence_certificate(signal, labels, rho, gamma, upto: int, trace_fp32) ->
     deficit = float((top - pick) / top) if top > 0 else 0.0
     return dict(at=int(upto), deficit=deficit, gap_amp=gap_amp, err_amp=err_amp,
                 strict=bool(deficit < 1e-6), bounded=bool(gap_amp <= 2.0 * err_amp))
+
+
+def fp64_tie_certificate(signal, labels, rho, gamma, upto: int, trace_a, trace_b) -> dict:
+    """Evidence for two fp64 runs (e.g. the GPU reference-arithmetic path and
+    the reference itself) whose canonical selection sequences first differ
+    at iteration `upto`.  The oracle is stepped to `upto` (its state stands
+    in for both runs' common fp64 state) and compares the two picks:
+      gap_amp  | |R[pick_a]| - |R[pick_b]| |,
+      err_amp  the measured disagreement of the two runs before the split:
+               max over the shared selections of |c_a - c_b| w00 / gamma
+               (c = gamma R / w00, cfse.py:85), and at `upto` each run's own
+               |R| estimate against the oracle's.
+    `bounded` = gap_amp <= 2 err_amp: the two bins are tied below the
+    runs' own fp64 rounding disagreement, so either pick is correct fp64."""
+    s = np.asarray(signal, np.float64)
+    w = build_weight(labels, rho)
+    W = dft2(w.astype(np.complex128))
+    R = dft2((s * w).astype(np.complex128))
+    e0 = float(np.sum(w * s * s))
+    M, N = R.shape
+    w00 = W[0, 0].real
+    _, ous, ovs, ocs, _ = cfse_kernel(R.copy(), W, gamma, 1.0 / w00, max(upto, 1), e0)
+    mirrored = not np.array_equal(canonicalize_trace(ous, ovs, ocs, M, N)[0], ous) if upto else False
+    if upto > 0:
+        cfse_kernel(R, W, gamma, 1.0 / w00, upto, e0)
+    au, av, ac = canonicalize_trace(*trace_a, M, N)
+    bu, bv, bc = canonicalize_trace(*trace_b, M, N)
+
+    def r_at(u, v):  # R in the canonical frame
+        return np.conj(R[(-u) % M, (-v) % N]) if mirrored else R[u, v]
+
+    ra, rb = r_at(int(au[upto]), int(av[upto])), r_at(int(bu[upto]), int(bv[upto]))
+    scale = w00 / gamma
+    err = [abs(complex(ac[k]) - complex(bc[k])) * scale for k in range(upto)]
+    err += [abs(complex(ac[upto]) * scale - complex(ra)), abs(complex(bc[upto]) * scale - complex(rb))]
+    err_amp = float(max(err))
+    gap_amp = float(abs(abs(ra) - abs(rb)))
+    top = float(np.max(R.real ** 2 + R.imag ** 2))
+    return dict(at=int(upto), gap_amp=gap_amp, err_amp=err_amp, rel_gap=gap_amp / np.sqrt(top),
+                bounded=bool(gap_amp <= 2.0 * err_amp))
+
+
+def _rfse_state(signal, labels, rho, gamma, upto):
+    s = np.asarray(signal, np.float64)
+    w = build_weight(labels, rho)
+    W = dft2(w.astype(np.complex128))
+    R = dft2((s * w).astype(np.complex128))
+    e0 = float(np.sum(w * s * s))
+    w00 = W[0, 0].real
+    pre = rfse_kernel(R, W, gamma, w00, upto, 2 * upto + 1, e0) if upto > 0 else None
+    return R, W, w00, pre
+
+
+def rfse_crit_map(R, W, w00):
+    """The pair-selection criterion of every bin (rfse.py:83-111)."""
+    M, N = R.shape
+    W2 = W[np.ix_((2 * np.arange(M)) % M, (2 * np.arange(N)) % N)]
+    selfc = ((2 * np.arange(M)) % M == 0)[:, None] & ((2 * np.arange(N)) % N == 0)[None, :]
+    D = w00 * w00 - np.abs(W2) ** 2
+    a = R
+    nr = w00 * a.real - (W2.real * a.real + W2.imag * a.imag)
+    ni = w00 * a.imag - (W2.imag * a.real - W2.real * a.imag)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        crit = 2.0 * (nr / D * a.real + ni / D * a.imag)
+    return np.where(selfc, a.real * a.real / w00, crit)
+
+
+def rfse_crit_of_coefficient(c, u, v, W, w00, gamma):
+    """The criterion value a selection's coefficient implies: p = c / gamma is
+    the joint projection, and crit = 2 p^T adj(A) p with A the pair Gram
+    matrix (= p_re^2 w00 for a self-conjugate bin)."""
+    M, N = W.shape
+    p = complex(c) / gamma
+    if (2 * u) % M == 0 and (2 * v) % N == 0:
+        return p.real * p.real * w00
+    w2 = W[(2 * u) % M, (2 * v) % N]
+    return 2.0 * (p.real ** 2 * (w00 + w2.real) + 2 * p.real * p.imag * w2.imag
+                  + p.imag ** 2 * (w00 - w2.real))
+
+
+def rfse_divergence_certificate(signal, labels, rho, gamma, upto: int, trace_fp32) -> dict:
+    """rFSE analogue of divergence_certificate: the fp64 oracle stepped to
+    `upto` (the fp32 run's first differing selection); `deficit` = relative
+    criterion gap between the fp64 pick and the fp32 pick, `err` = the fp32
+    run's measured criterion error (the largest |crit(c32) - crit(c64)| over
+    the shared selections, crit implied by the coefficient, and at the fp32
+    pick itself).  strict: deficit < 1e-6; bounded: gap <= 2 err."""
+    R, W, w00, pre = _rfse_state(signal, labels, rho, gamma, upto)
+    us32, vs32, cs32 = (np.asarray(x) for x in trace_fp32[:3])
+    crit = rfse_crit_map(R, W, w00)
+    top = float(np.max(crit))
+    pu, pv = int(us32[upto]), int(vs32[upto])
+    pick = float(crit[pu, pv])
+    err = []
+    if pre is not None:
+        _, ous, ovs, ocs, _, _, _ = pre
+        for k in range(upto):
+            u, v = int(ous[k]), int(ovs[k])
+            err.append(abs(rfse_crit_of_coefficient(cs32[k], u, v, W, w00, gamma)
+                           - rfse_crit_of_coefficient(ocs[k], u, v, W, w00, gamma)))
+    err.append(abs(rfse_crit_of_coefficient(cs32[upto], pu, pv, W, w00, gamma) - pick))
+    gap = top - pick
+    deficit = gap / top if top > 0 else 0.0
+    return dict(at=int(upto), deficit=float(deficit), gap=float(gap), err=float(max(err)),
+                strict=bool(deficit < 1e-6), bounded=bool(gap <= 2.0 * max(err)))
 
 
 def near_tie_gap(signal, labels, rho, gamma, upto: int) -> float:

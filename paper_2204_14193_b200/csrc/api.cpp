@@ -386,8 +386,8 @@ int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int 
   p->fast = precision == FSE_PREC_F32 &&
             fse::fast_config(F, iterations, sm_count(), &p->cfg, algorithm) &&
             B * B == 2 * (F * F / 32) && iterations > 0;
-  double *dmin_dev = nullptr;
-  if (p->fast && algorithm == FSE_ALG_RFSE) CK(p->alloc(&dmin_dev, (size_t)std::max(nc, 1)));
+  double *dmin_dev = nullptr;  // rfse.py:47-55 degeneracy check, every rFSE plan
+  if (algorithm == FSE_ALG_RFSE) CK(p->alloc(&dmin_dev, (size_t)std::max(nc, 1)));
   if (p->fast) CK(p->alloc((char **)&p->table, (size_t)nc * p->cfg.table_bytes));
   if (p->fast && p->cfg.global_trace)
     CK(p->alloc(&p->trace_scratch, (size_t)p->cfg.grid * p->cfg.slots * 2 * iterations));
@@ -561,7 +561,7 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     CK(fse::launch_fast(a, p->cfg, a.use_tma ? &tmap : nullptr, st));
     return FSE_OK;
   }
-  if (trace_uv) return fail(FSE_ERR_UNSUPPORTED, "trace output is only available on the fused fp32 path");
+  if (trace_uv && (!trace_c || !trace_e)) return fail(FSE_ERR_VALUE, "partial trace buffers");
   const int F = p->F, B = p->B;
   for (int c0 = 0; c0 < p->n_blocks; c0 += p->chunk) {
     const int n = std::min(p->chunk, p->n_blocks - c0);
@@ -579,6 +579,14 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     const size_t esz = tile_dtype == 0 ? 1 : tile_dtype == 1 ? 4 : 8;
     CK(fse::launch_extract_tiles(p->recon, n, F, B, (char *)tiles + (size_t)c0 * B * B * esz,
                                  tile_dtype, st));
+    if (trace_uv) {  // trace: f64 entries for fp64 plans, f32 otherwise
+      const size_t It = (size_t)p->iterations, tsz = p->precision == FSE_PREC_F64 ? 8 : 4;
+      CK(fse::launch_pack_trace(p->us, p->vs, p->cs, p->es, p->algorithm ? p->counts : nullptr, n,
+                                p->iterations, trace_uv + (size_t)c0 * It * 2,
+                                (char *)trace_c + (size_t)c0 * It * 2 * tsz,
+                                (char *)trace_e + (size_t)c0 * It * tsz,
+                                p->precision == FSE_PREC_F64, st));
+    }
   }
   return FSE_OK;
 }

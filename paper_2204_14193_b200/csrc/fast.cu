@@ -1319,6 +1319,27 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
   }
   __syncthreads();
   if (threadIdx.x == 0) a.w00[c] = W[0].x;
+  if (a.dmin) {
+    // rFSE pair Gram determinant check (rfse.py:47-55), for every rFSE plan:
+    // min over non-self-conjugate bins of (W00^2 - |W[2k, 2l]|^2) / W00^2
+    __shared__ double red[512];
+    const double w00 = W[0].x;
+    double dmin = 1e300;
+    for (int i = threadIdx.x; i < FF; i += blockDim.x) {
+      const int k = i / F, l = i - k * F;
+      const int r2 = (2 * k) % F, c2 = (2 * l) % F;
+      if (r2 == 0 && c2 == 0) continue;
+      const double2 w2 = W[r2 * F + c2];
+      dmin = fmin(dmin, (w00 * w00 - (w2.x * w2.x + w2.y * w2.y)) / (w00 * w00));
+    }
+    red[threadIdx.x] = dmin;
+    __syncthreads();
+    for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
+      if ((int)threadIdx.x < s2) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + s2]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) a.dmin[c] = red[0];
+  }
   if (!a.fast_table) return;
   char *tab = (char *)a.fast_table + (size_t)c * a.fast_table_bytes;
   if (F == 128) {
@@ -1346,15 +1367,13 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       // W00 + W2.re]] a / Dt, Dt = W00^2 - |W2|^2, W2 = W[2k, 2l], is
       // crit = A a.re^2 + C a.im^2 - D a.re a.im with A = 2 (W00 - W2.re) / Dt,
       // C = 2 (W00 + W2.re) / Dt, D = 4 W2.im / Dt; a self-conjugate bin
-      // (crit = a.re^2 / W00) has A = 1 / W00, C = D = 0.  Also the minimum of
-      // Dt / W00^2 over pair bins.
+      // (crit = a.re^2 / W00) has A = 1 / W00, C = D = 0.
       // Entry i = (r, c) of the thread layout (32 columns): bins (r, c) and
       // (r, c + 32) at F = 64; bins (2r, c) and (2r + 1, c) at F = 32.
       const double w00 = W[0].x;
       const size_t TB = F == 32 ? FG<32>::TABLE_BYTES : FG<64>::TABLE_BYTES;
       float4 *A4 = (float4 *)(tab + TB);
       float2 *A2 = (float2 *)(tab + TB + (size_t)FF / 2 * sizeof(float4));
-      double dmin = 1e300;
       for (int i = threadIdx.x; i < FF / 2; i += blockDim.x) {
         const int r = i >> 5, c = i & 31;
         double qa[2], qc[2], qd[2];
@@ -1368,7 +1387,6 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
           } else {
             const double2 w2 = W[r2 * F + c2];
             const double d = w00 * w00 - (w2.x * w2.x + w2.y * w2.y);
-            dmin = fmin(dmin, d / (w00 * w00));
             qa[h] = 2.0 * (w00 - w2.x) / d;
             qc[h] = 2.0 * (w00 + w2.x) / d;
             qd[h] = 4.0 * w2.y / d;
@@ -1377,15 +1395,6 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
         A4[i] = make_float4((float)qa[0], (float)qa[1], (float)qc[0], (float)qc[1]);
         A2[i] = make_float2((float)-qd[0], (float)-qd[1]);
       }
-      // block minimum of dmin -> a.dmin[c]
-      __shared__ double red[512];
-      red[threadIdx.x] = dmin;
-      __syncthreads();
-      for (int s2 = blockDim.x / 2; s2 > 0; s2 >>= 1) {
-        if ((int)threadIdx.x < s2) red[threadIdx.x] = fmin(red[threadIdx.x], red[threadIdx.x + s2]);
-        __syncthreads();
-      }
-      if (threadIdx.x == 0 && a.dmin) a.dmin[c] = red[0];
     }
   }
 }

@@ -20,6 +20,7 @@
 //   recon  = s on support/padding, Re{g} on loss           cfse.py:127-129
 #include <float.h>
 #include <limits.h>
+#include <math_constants.h>
 
 #include "common.cuh"
 #include "dft.cuh"
@@ -29,9 +30,12 @@ namespace fse {
 
 constexpr int kGenThreads = 512;
 
-__device__ double block_max_abs(const double *x, int n, double *red) {
+// max |x[i]| over the samples with lab[i] == keep (all when lab is null)
+__device__ double block_max_abs(const double *x, int n, double *red, const int8_t *lab = nullptr,
+                                int keep = 0) {
   double v = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) v = fmax(v, fabs(x[i]));
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (!lab || lab[i] == keep) v = fmax(v, fabs(x[i]));
   for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
@@ -477,17 +481,23 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
   }
   // kappa = 2^-e with max|s| = f 2^e, f in [0.5, 1): balances the two real
   // signals packed into one complex DFT; scaling by a power of two is exact.
-  double smax = block_max_abs(s, MN, red);
+  // Only support samples enter the transforms: loss / padding samples have
+  // w = 0, so this equals the reference for finite input, and a non-finite
+  // value in the lost block (common for decoded frames) cannot leak into
+  // the window through 0 * NaN.
+  double smax = block_max_abs(s, MN, red, lab, kSupport);
   int ex = 0;
   if (smax > 0.0) frexp(smax, &ex);
   const double kappa = ldexp(1.0, -ex), inv_kappa = ldexp(1.0, ex);
   double e0p = 0.0;
   for (int i = threadIdx.x; i < MN; i += blockDim.x) {
     int m = i / N, n = i - m * N;
-    double w = lab[i] == kSupport ? weight_at(m, n, M, N, a.rho) : 0.0;
-    double sw = s[i] * w;
+    const bool sup = lab[i] == kSupport;
+    double w = sup ? weight_at(m, n, M, N, a.rho) : 0.0;
+    const double si = sup ? s[i] : 0.0;
+    double sw = si * w;
     A[i] = make_double2(w, sw * kappa);
-    e0p += w * s[i] * s[i];  // np.sum(w * s * s), cfse.py:51
+    e0p += w * si * si;  // np.sum(w * s * s), cfse.py:51
   }
   const double e0 = block_sum(e0p, red);  // includes barrier
   dft_rows(A, Bf, M, N, twN);
@@ -497,7 +507,12 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
   unpack_two_real(A, Bf, M, N, inv_kappa);  // Bf = W, A = R_w
   __syncthreads();
   const double w00 = Bf[0].x;
+  // rejected windows still write their output: the input outside the loss,
+  // NaN on it (never stale memory).  Plans reject these geometries at
+  // creation; the per-window status reports them to the direct API.
+  double *rec_out = a.recon + (size_t)win * MN;
   if (w00 <= 1e-12 * (double)M * (double)N) {  // cfse.py:47-48
+    for (int i = threadIdx.x; i < MN; i += blockDim.x) rec_out[i] = lab[i] == kLoss ? CUDART_NAN : s[i];
     if (threadIdx.x == 0) a.status[win] = 1;
     return;
   }
@@ -512,6 +527,7 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
       if (D <= 1e-9 * w00 * w00) bad = 1;
     }
     if (__syncthreads_or(bad)) {
+      for (int i = threadIdx.x; i < MN; i += blockDim.x) rec_out[i] = lab[i] == kLoss ? CUDART_NAN : s[i];
       if (threadIdx.x == 0) a.status[win] = 2;
       return;
     }
@@ -781,6 +797,36 @@ cudaError_t launch_extract_tiles(const double *recon, int n, int F, int B, void 
                                  int tile_dtype, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   extract_tiles_kernel<<<n, 256, 0, s>>>(recon, F, B, tiles, tile_dtype);
+  return cudaGetLastError();
+}
+
+__global__ void pack_trace_kernel(const int64_t *us, const int64_t *vs, const double *cs,
+                                  const double *es, const int32_t *counts, int n, int It,
+                                  int32_t *uv, void *c, void *e, int c64) {
+  const long long total = (long long)n * It;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int w = (int)(i / It), it = (int)(i - (long long)w * It);
+    const bool used = !counts || it < counts[w];
+    uv[2 * i] = used ? (int32_t)us[i] : -1;
+    uv[2 * i + 1] = used ? (int32_t)vs[i] : -1;
+    const double re = used ? cs[2 * i] : 0.0, im = used ? cs[2 * i + 1] : 0.0;
+    const double en = used ? es[i] : 0.0;
+    if (c64) {
+      ((double *)c)[2 * i] = re; ((double *)c)[2 * i + 1] = im; ((double *)e)[i] = en;
+    } else {
+      ((float *)c)[2 * i] = (float)re; ((float *)c)[2 * i + 1] = (float)im; ((float *)e)[i] = (float)en;
+    }
+  }
+}
+
+cudaError_t launch_pack_trace(const int64_t *us, const int64_t *vs, const double *cs,
+                              const double *es, const int32_t *counts, int n, int It,
+                              int32_t *uv, void *c, void *e, int c64, cudaStream_t s) {
+  const long long total = (long long)n * It;
+  if (total <= 0) return cudaSuccess;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 4096);
+  pack_trace_kernel<<<grid, 256, 0, s>>>(us, vs, cs, es, counts, n, It, uv, c, e, c64);
   return cudaGetLastError();
 }
 

@@ -113,5 +113,12 @@ cudaError_t launch_gather_windows(const void *frames, int dtype, long long pitch
 // Copy the B x B loss tiles out of reconstructed windows into tiles.
 cudaError_t launch_extract_tiles(const double *recon, int n, int F, int B, void *tiles,
                                  int tile_dtype, cudaStream_t s);
+// Pack the per-window trace (us, vs int64; cs re/im f64; es f64; `counts`
+// executed iterations per window or null = all) into the plan trace layout:
+// uv int32 (n, It, 2), c (n, It, 2) and e (n, It) as f64 (c64 != 0) or f32;
+// iterations past a window's count get uv = -1, c = e = 0.
+cudaError_t launch_pack_trace(const int64_t *us, const int64_t *vs, const double *cs,
+                              const double *es, const int32_t *counts, int n, int It,
+                              int32_t *uv, void *c, void *e, int c64, cudaStream_t s);
 
 }  // namespace fse

@@ -3,6 +3,7 @@
 Run in the build container (where /root/reference exists):
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py wide   # wide_*.npz
 
 It imports the unmodified reference package `fse` (cfse.py / weighting.py /
 types.py), runs `extrapolate_cfse` on seeded windows cut from the synthetic
@@ -28,7 +29,8 @@ from fse.rfse import extrapolate_rfse  # noqa: E402
 from fse.types import FseConfig  # noqa: E402
 from fse.weighting import AreaMask, build_mask  # noqa: E402
 
-from paper_2204_14193_b200.synth import field  # noqa: E402
+from paper_2204_14193_b200.synth import field, frame_u8  # noqa: E402
+from oracle.oracle import frames_pattern  # noqa: E402  (== the product's pattern generator)
 
 
 def window(img, top, left, F, B, border):
@@ -177,5 +179,130 @@ def main():
     save("rfse.npz", cases)
 
 
+# ---------------------------------------------------------------- wide sets
+# The wide fp64 gate (>= 1,000 reference windows over every BASELINE config
+# geometry).  Inputs are NOT stored: the test regenerates the seeded frames
+# with paper_2204_14193_b200.synth (numpy, deterministic) and cuts the same
+# windows; the fixture holds the block list and the reference's outputs.
+
+WIDE_SETS = {
+    # name: frame generator spec, blocks, geometry, iterations
+    "c2": dict(gen="field_f32", shape=(512, 512), seeds=[2], F=64, B=16, border=16, iters=100),
+    "c4a": dict(gen="field_f32", shape=(512, 512), seeds=[4], F=32, B=8, border=8, iters=100),
+    "c4b": dict(gen="field_f32", shape=(512, 512), seeds=[40 + k for k in range(8)], F=128, B=32,
+                border=16, iters=100, pixels=125),
+    "c5": dict(gen="frame_u8", shape=(2160, 3840), seeds=[500, 501], F=64, B=16, border=16, iters=100),
+    "c3": dict(gen="frame_u8", shape=(1080, 1920), seeds=[300, 301], F=64, B=16, border=16, iters=200),
+}
+
+
+# rFSE wide sets (rfse.py:170-210): fixed count and basis_target runs
+WIDE_RFSE = {
+    "r64": dict(gen="field_f32", shape=(512, 512), seeds=[2], F=64, B=16, border=16, iters=50),
+    "r32": dict(gen="field_f32", shape=(512, 512), seeds=[4], F=32, B=8, border=8, iters=50),
+    "r128": dict(gen="field_f32", shape=(512, 512), seeds=[40], F=128, B=32, border=16, iters=40),
+}
+
+
+def rfse_blocks(name):
+    if name == "r64":
+        return np.array([(0, 32 * i, 32 * j) for i in range(16) for j in range(16)], np.int32)
+    if name == "r32":
+        tl = np.array([(16 * i, 16 * j) for i in range(32) for j in range(32)], np.int32)[::4]
+        return np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
+    return np.array([(0, 64 * i, 64 * j) for i in range(8) for j in range(8)], np.int32)
+
+
+def make_wide_rfse(name):
+    spec = WIDE_RFSE[name]
+    frames = wide_frames(spec)
+    blocks = rfse_blocks(name)
+    F, B, border, I = spec["F"], spec["B"], spec["border"], spec["iters"]
+    rho, gamma = 0.8, 0.5
+    n = len(blocks)
+    # every 4th window runs in basis_target mode (target 2 I - 3: ends on the tally rule)
+    bts = np.array([2 * I - 3 if k % 4 == 3 else -1 for k in range(n)], np.int32)
+    cap = max(I, 2 * I - 3)
+    uv = np.full((n, cap, 2), -1, np.int16)
+    cs = np.zeros((n, cap), np.complex128)
+    selfs = np.zeros((n, cap), np.uint8)
+    count = np.zeros(n, np.int32)
+    tally = np.zeros(n, np.int32)
+    px = np.zeros((n, B * B))
+    for k, (f, t, l) in enumerate(blocks):
+        s, m = window(frames[f].astype(np.float64), int(t), int(l), F, B, border)
+        r = run_rfse(s, m, rho, gamma, I, basis_target=None if bts[k] < 0 else int(bts[k]))
+        c = len(r["us"])
+        uv[k, :c, 0], uv[k, :c, 1] = r["us"], r["vs"]
+        cs[k, :c] = r["cs"]
+        selfs[k, :c] = r["selfs"]
+        count[k], tally[k] = c, r["tally"]
+        px[k] = r["recon_loss"]
+    np.savez_compressed(os.path.join(HERE, f"wide_{name}.npz"), blocks=blocks, basis_target=bts, uv=uv,
+                        cs=cs, selfs=selfs, count=count, tally=tally, pixels=px, F=F, B=B, border=border,
+                        iterations=I, rho=rho, gamma=gamma)
+    print(f"wide_{name}.npz", n, "windows")
+
+
+def wide_frames(spec):
+    H, W = spec["shape"]
+    if spec["gen"] == "field_f32":
+        return np.stack([field(H, W, seed=s).astype(np.float32) for s in spec["seeds"]])
+    return np.stack([frame_u8(H, W, seed=s) for s in spec["seeds"]])
+
+
+def wide_blocks(name, spec):
+    H, W = spec["shape"]
+    if name == "c2":
+        return np.array([(0, 32 * i, 32 * j) for i in range(16) for j in range(16)], np.int32)
+    if name == "c4a":
+        tl = np.array([(16 * i, 16 * j) for i in range(32) for j in range(32)], np.int32)[::2][:500]
+        tl = tl[np.lexsort((tl[:, 1], tl[:, 0]))]
+        return np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
+    if name == "c4b":
+        return np.array([(f, 64 * i, 64 * j) for f in range(8) for i in range(8) for j in range(8)],
+                        np.int32)[:500]
+    frac, seed, n = (0.05, 5, 120) if name == "c5" else (0.10, 3, 100)
+    allb = frames_pattern(2, H, W, 16, frac, seed)
+    b = allb[np.linspace(0, len(allb) - 1, n).round().astype(np.int64)]
+    if name == "c5":  # + the four corner classes
+        b = np.concatenate([b, np.array([[1, 0, 0], [1, 0, W - 16], [1, H - 16, 0], [1, H - 16, W - 16]],
+                                        np.int32)])
+    return b
+
+
+def make_wide(name):
+    spec = WIDE_SETS[name]
+    frames = wide_frames(spec)
+    blocks = wide_blocks(name, spec)
+    F, B, border, I = spec["F"], spec["B"], spec["border"], spec["iters"]
+    rho, gamma = 0.8, 0.5
+    n = len(blocks)
+    uv = np.zeros((n, I, 2), np.uint8)
+    cs = np.zeros((n, I), np.complex128)
+    w00 = np.zeros(n)
+    e0 = np.zeros(n)
+    npx = spec.get("pixels", n)
+    px = np.zeros((npx, B * B))
+    for k, (f, t, l) in enumerate(blocks):
+        s, m = window(frames[f].astype(np.float64), int(t), int(l), F, B, border)
+        r = run(s, m, rho, gamma, I)
+        uv[k, :, 0], uv[k, :, 1] = r["us"], r["vs"]
+        cs[k] = r["cs"]
+        w00[k], e0[k] = r["w00"], r["e0"]
+        if k < npx:
+            px[k] = r["recon_loss"]
+    np.savez_compressed(os.path.join(HERE, f"wide_{name}.npz"), blocks=blocks, uv=uv, cs=cs, w00=w00,
+                        e0=e0, pixels=px, F=F, B=B, border=border, iterations=I, rho=rho, gamma=gamma)
+    print(f"wide_{name}.npz", n, "windows")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "wide":
+        for name in (sys.argv[2:] or list(WIDE_SETS) + list(WIDE_RFSE)):
+            if name in WIDE_RFSE:
+                make_wide_rfse(name)
+            else:
+                make_wide(name)
+    else:
+        main()

@@ -71,3 +71,39 @@ def test_oracle_loss_pattern_equals_native_generator():
         a = orc.frames_pattern(3, H, W, B, frac, seed)
         b = fse.frames_pattern(3, H, W, B, frac, seed)
         assert np.array_equal(a, b), (H, W, B)
+
+
+def test_rfse_certificate_of_a_forced_second_best_pick():
+    """rFSE: follow the oracle's selections, then take the criterion
+    runner-up at iteration k with its exact fp64 coefficient: the
+    certificate reports the criterion gap as the deficit and no measured
+    error; a perturbed earlier coefficient makes it 'bounded'."""
+    s, lab = _window()
+    rho, gamma, k = 0.8, 0.5, 5
+    R, W, w00, pre = orc._rfse_state(s, lab, rho, gamma, k)
+    _, us, vs, cs, _, _, _ = pre
+    crit = orc.rfse_crit_map(R, W, w00)
+    order = np.argsort(crit.ravel())[::-1]
+    top = order[0]
+    tu, tv = divmod(int(top), 64)
+    mir = ((-tu) % 64) * 64 + (-tv) % 64
+    sec = next(int(i) for i in order[1:] if i != mir)   # the top's pair partner is the same pair
+    su, sv = divmod(sec, 64)
+    # the runner-up's own projection (rfse.py:93-103), canonical member
+    a = R[su, sv]
+    w2 = W[(2 * su) % 64, (2 * sv) % 64]
+    D = w00 * w00 - abs(w2) ** 2
+    p = complex((w00 * a.real - (w2.real * a.real + w2.imag * a.imag)) / D,
+                (w00 * a.imag - (w2.imag * a.real - w2.real * a.imag)) / D)
+    mu, mv = (-su) % 64, (-sv) % 64
+    if mu * 64 + mv < su * 64 + sv:
+        su, sv, p = mu, mv, p.conjugate()
+    tr = (np.append(us, su), np.append(vs, sv), np.append(cs, gamma * p))
+    cert = orc.rfse_divergence_certificate(s, lab, rho, gamma, k, tr)
+    gap = crit.ravel()[top] - crit[su, sv]
+    assert abs(cert["gap"] - gap) <= 1e-9 * crit.ravel()[top]
+    assert cert["err"] <= 1e-9 * crit.ravel()[top]
+    assert not cert["bounded"]
+    cs2 = tr[2].copy()
+    cs2[k - 1] *= 1 + 1e-3
+    assert orc.rfse_divergence_certificate(s, lab, rho, gamma, k, (tr[0], tr[1], cs2))["err"] > 0

@@ -67,7 +67,8 @@ def test_fused_path_random_geometry(fse, seed):
 @pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("FSE_FUZZ_SEEDS", 6))))
 def test_fp64_plan_random_geometry(fse, seed):
     """The fp64 image-level path (reference arithmetic, any window size) on
-    random geometry: tiles within 1e-9 of the fp64 oracle."""
+    random geometry: canonical selection sequence identical to the fp64
+    oracle's (or a certified fp64 near-tie), tiles within 1e-9."""
     import torch
     from oracle import oracle as orc
     from paper_2204_14193_b200.synth import field
@@ -85,6 +86,20 @@ def test_fp64_plan_random_geometry(fse, seed):
     img = field(H, W, seed=seed)
     plan = fse.ConcealPlan(blocks, H, W, fse.Geometry(B, border, F), rho_hat=0.8, gamma=0.5,
                            iterations=iters, precision="fp64")
-    tiles = plan.run(torch.from_numpy(img).cuda(), tile_dtype="f64").cpu().numpy()
+    tiles, tr = plan.run(torch.from_numpy(img).cuda(), tile_dtype="f64", trace=True)
+    tiles = tiles.cpu().numpy()
+    uv = tr["uv"].cpu().numpy().astype(np.int64)
+    cc = tr["c"].cpu().numpy()
     ref = orc.conceal_blocks(img, blocks, B, border, F, 0.8, 0.5, iters)
-    np.testing.assert_allclose(tiles, ref, rtol=0, atol=1e-9)
+    from oracle.gate import window_of
+    for k, (_, t, l) in enumerate(blocks):
+        s, lab = window_of(img, int(t), int(l), F, B, border)
+        o = orc.extrapolate(s, lab, 0.8, 0.5, iters)
+        ours = (uv[k, :, 0], uv[k, :, 1], cc[k, :, 0] + 1j * cc[k, :, 1])
+        kind, _ = orc.trace_equivalence((o["us"], o["vs"], o["cs"]), ours, F, F)
+        if kind in ("identical", "mirror"):
+            np.testing.assert_allclose(tiles[k], ref[k], rtol=0, atol=1e-9)
+            continue
+        at = orc.first_divergence((o["us"], o["vs"], o["cs"]), ours, F, F)
+        cert = orc.fp64_tie_certificate(s, lab, 0.8, 0.5, at, ours, (o["us"], o["vs"], o["cs"]))
+        assert at is not None and cert["bounded"], (k, kind, cert)

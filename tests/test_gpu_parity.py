@@ -39,7 +39,7 @@ def test_extrapolate_fp64_matches_reference(fse, c):
     cs = np.array([t.coefficient for t in r.trace], np.complex128)
     es = np.array([t.residual_energy for t in r.trace])
     kind, info = orc.trace_equivalence(_golden.trace(c), (us, vs, cs), M, N)
-    assert kind != "diverged", (kind, info)
+    assert kind in ("identical", "mirror"), (kind, info)  # mirror-pair swaps fail
     if c["iterations"]:
         np.testing.assert_allclose(es, c["es"], rtol=1e-9, atol=1e-9 * c["e0"])
     if "model" in c:
@@ -59,7 +59,7 @@ def test_fp64_canonical_fraction(fse):
         k, _ = orc.trace_equivalence(_golden.trace(c), tr, M, N)
         kinds[k] = kinds.get(k, 0) + 1
     print("fp64 trace agreement vs reference:", kinds)
-    assert "diverged" not in kinds
+    assert set(kinds) <= {"identical", "mirror"}, kinds
 
 
 def test_cfse_kernel_bitwise_on_reference_spectra(fse):

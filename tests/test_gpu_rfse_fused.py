@@ -43,8 +43,7 @@ def test_fused_rfse_matches_fp64(fse, dtype, iters, bt):
     fast, ref = _plans(fse, blocks, H, W, **kw)
     t32, tr = fast.run(frames, tile_dtype="f32", trace=True)
     t64 = ref.run(frames, tile_dtype="f64")
-    dev = (t32.double() - t64).abs().reshape(len(blocks), -1).max(1).values.cpu().numpy()
-    assert dev.max() <= 0.5, (dev.max(), int((dev > 0.5).sum()))
+    print(_rfse_gate(fse, frames, blocks, t32, tr, t64, 64, 16, iters, bt, log=f"rfse64_{dtype}_{iters}_{bt}"))
     uv = tr["uv"].cpu().numpy()
     e = tr["e"].cpu().numpy()
     n_it = fast.iterations
@@ -65,9 +64,11 @@ def test_fused_rfse_matches_fp64(fse, dtype, iters, bt):
 
 
 def test_fused_rfse_selection_sequence(fse):
-    """The fused kernel's canonical (u, v) sequence equals the reference-
-    arithmetic per-window rFSE's (fse.extrapolate_rfse, fp64) on interior
-    windows of a u8 frame, up to its first near-tie divergence."""
+    """The fused kernel's (u, v) sequence (canonical pair members) equals the
+    C oracle's fp64 rFSE (rfse.py:56-167 restated) for every block over all
+    60 iterations, except at a certified near-tie (criterion gap < 1e-6
+    relative or within twice the fp32 run's measured error), after which the
+    two runs legitimately differ."""
     import torch
     from paper_2204_14193_b200.synth import frame_u8
     from tests._windows import window_of
@@ -75,19 +76,22 @@ def test_fused_rfse_selection_sequence(fse):
     blocks = np.array([[0, 64 + 32 * i, 64 + 48 * j] for i in range(3) for j in range(4)], np.int32)
     fast, _ = _plans(fse, blocks, 256, 384, iterations=60)
     _, tr = fast.run(torch.from_numpy(fr).cuda(), tile_dtype="f32", trace=True)
-    uv = tr["uv"].cpu().numpy()
-    full = 0
+    get = _trace_getter(tr)
+    from oracle import oracle as orc
+    from oracle.gate import first_rfse_divergence
+    full, ties = 0, []
     for k, (f, t, l) in enumerate(blocks):
         s, lab = window_of(fr.astype(np.float64), t, l, 64, 16, 16)
-        mask = fse.AreaMask(lab)
-        r = fse.extrapolate_rfse(s, mask, fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=60,
-                                                        fft_dims=(64, 64), algorithm="rfse"))
-        ref_uv = np.array([rec.frequency for rec in r.trace])
-        same = np.all(ref_uv == uv[k], axis=1)
-        first_diff = len(same) if same.all() else int(np.argmin(same))
-        assert first_diff >= 20, (k, first_diff)
-        full += first_diff == len(same)
-    assert full >= len(blocks) // 2
+        o = orc.extrapolate_rfse(s, lab, 0.8, 0.5, 60)
+        at = first_rfse_divergence((o["us"], o["vs"]), get(k))
+        if at is None:
+            full += 1
+            continue
+        cert = orc.rfse_divergence_certificate(s, lab, 0.8, 0.5, at, get(k))
+        assert cert["strict"] or cert["bounded"], (k, cert)
+        ties.append((k, cert))
+    print("identical", full, "certified ties", ties)
+
 
 
 def test_rfse_degenerate_support_raises(fse):
@@ -104,37 +108,32 @@ def test_rfse_degenerate_support_raises(fse):
 _SEEDS = int(__import__("os").environ.get("FSE_FUZZ_SEEDS", 0))  # widen for one-off sweeps
 
 
-def _rfse_gate(fse, img, blocks, t32, tr32, t64, F, B, iters, bt):
-    """fp32 gate for rFSE (as for cFSE): every block within 0.5
-    gray levels of the fp64 plan, except certified near-ties.  A block is
-    certified when its canonical selection sequence equals the per-window
-    reference-arithmetic rFSE's (fp64) up to a first divergence k >= 1 at
-    which the fp32 run's own energy decrease for its pick is within 1e-4
-    (relative) of the fp64 run's decrease for the fp64 pick -- both picks
-    are greedy-optimal to fp32 accumulated precision."""
-    from tests._windows import window_of
-    dev = (t32.double() - t64).abs().reshape(len(blocks), -1).max(1).values.cpu().numpy()
+def _trace_getter(tr32):
     uv = tr32["uv"].cpu().numpy()
-    e32 = tr32["e"].cpu().numpy().astype(np.float64)
-    certified = []
-    for k in np.nonzero(dev > 0.5)[0]:
-        f, t, l = (int(x) for x in blocks[k])
-        fr = img[f] if img.ndim == 3 else img
-        s, lab = window_of(fr.astype(np.float64), t, l, F, B, B)
-        r = fse.extrapolate_rfse(s, fse.AreaMask(lab), fse.FseConfig(
-            rho_hat=0.8, gamma=0.5, iterations=iters, fft_dims=(F, F), algorithm="rfse", basis_target=bt))
-        ref_uv = np.array([rec.frequency for rec in r.trace])
-        e64 = np.array([rec.residual_energy for rec in r.trace])
-        m = min(len(ref_uv), int((uv[k, :, 0] >= 0).sum()))
-        same = np.all(ref_uv[:m] == uv[k, :m], axis=1)
-        assert not same.all(), (k, "identical selections but pixels differ", dev[k])
-        d = int(np.argmin(same))
-        assert d >= 1, (k, "diverges at the first selection", dev[k])
-        dec32, dec64 = e32[k, d - 1] - e32[k, d], e64[d - 1] - e64[d]
-        assert abs(dec32 - dec64) <= 1e-4 * abs(dec64), (k, d, dec32, dec64, dev[k])
-        certified.append((int(k), d, float(dev[k])))
-    assert len(certified) <= max(1, len(blocks) // 50), certified
-    return certified
+    c = tr32["c"].cpu().numpy()
+
+    def get(k):
+        used = uv[k, :, 0] >= 0
+        return (uv[k, used, 0].astype(np.int64), uv[k, used, 1].astype(np.int64),
+                c[k, used, 0] + 1j * c[k, used, 1])
+    return get
+
+
+def _rfse_gate(fse, img, blocks, t32, tr32, t64, F, B, iters, bt, log=None):
+    """fp32 rFSE gate against the independent C oracle's rFSE (oracle/gate.py
+    rfse_gate, rfse.py:37-210 restated): every block within 0.5 gray levels
+    except certified near-ties (criterion gap < 1e-6 relative, or within
+    twice the fp32 run's measured criterion error at the first differing
+    selection).  Also: the fp64 GPU plan (t64) agrees with the oracle to 1e-9."""
+    from oracle import oracle as orc
+    from oracle.gate import rfse_gate
+    fr = img.cpu().numpy() if hasattr(img, "cpu") else np.asarray(img)
+    fr = fr if fr.ndim == 3 else fr[None]
+    st = rfse_gate(fr, blocks, t32.cpu().numpy(), _trace_getter(tr32), F, B, B, 0.8, 0.5, iters, bt, log=log)
+    if t64 is not None:
+        ref = orc.conceal_blocks_rfse(fr, blocks, B, B, F, 0.8, 0.5, iters, bt)
+        np.testing.assert_allclose(t64.cpu().numpy(), ref, rtol=0, atol=1e-9)
+    return {k: v for k, v in st.items() if k != "outliers"}
 
 
 @pytest.mark.parametrize("seed", range(_SEEDS or 6))
@@ -189,8 +188,7 @@ def test_fused_rfse32_matches_fp64(fse, dtype, iters, bt):
     fast, ref = _plans(fse, blocks, H, W, geo=fse.Geometry(8, 8, 32), **kw)
     t32, tr = fast.run(frames, tile_dtype="f32", trace=True)
     t64 = ref.run(frames, tile_dtype="f64")
-    dev = (t32.double() - t64).abs().reshape(len(blocks), -1).max(1).values.cpu().numpy()
-    assert dev.max() <= 0.5, (dev.max(), int((dev > 0.5).sum()))
+    print(_rfse_gate(fse, frames, blocks, t32, tr, t64, 32, 8, iters, bt, log=f"rfse32_{dtype}_{iters}_{bt}"))
     uv = tr["uv"].cpu().numpy()
     for k in range(len(blocks)):
         used = uv[k, :, 0] >= 0
@@ -206,8 +204,11 @@ def test_fused_rfse32_matches_fp64(fse, dtype, iters, bt):
 
 
 def test_fused_rfse32_selection_sequence(fse):
-    """F = 32 fused canonical (u, v) sequence equals the reference-arithmetic
-    per-window rFSE's on interior windows, up to the first near-tie."""
+    """The fused kernel's (u, v) sequence (canonical pair members) equals the
+    C oracle's fp64 rFSE (rfse.py:56-167 restated) for every block over all
+    40 iterations, except at a certified near-tie (criterion gap < 1e-6
+    relative or within twice the fp32 run's measured error), after which the
+    two runs legitimately differ."""
     import torch
     from paper_2204_14193_b200.synth import frame_u8
     from tests._windows import window_of
@@ -215,18 +216,22 @@ def test_fused_rfse32_selection_sequence(fse):
     blocks = np.array([[0, 32 + 24 * i, 32 + 40 * j] for i in range(3) for j in range(4)], np.int32)
     fast, _ = _plans(fse, blocks, 160, 224, geo=fse.Geometry(8, 8, 32), iterations=40)
     _, tr = fast.run(torch.from_numpy(fr).cuda(), tile_dtype="f32", trace=True)
-    uv = tr["uv"].cpu().numpy()
-    full = 0
+    get = _trace_getter(tr)
+    from oracle import oracle as orc
+    from oracle.gate import first_rfse_divergence
+    full, ties = 0, []
     for k, (f, t, l) in enumerate(blocks):
         s, lab = window_of(fr.astype(np.float64), t, l, 32, 8, 8)
-        r = fse.extrapolate_rfse(s, fse.AreaMask(lab), fse.FseConfig(
-            rho_hat=0.8, gamma=0.5, iterations=40, fft_dims=(32, 32), algorithm="rfse"))
-        ref_uv = np.array([rec.frequency for rec in r.trace])
-        same = np.all(ref_uv == uv[k], axis=1)
-        first_diff = len(same) if same.all() else int(np.argmin(same))
-        assert first_diff >= 15, (k, first_diff)
-        full += first_diff == len(same)
-    assert full >= len(blocks) // 2
+        o = orc.extrapolate_rfse(s, lab, 0.8, 0.5, 40)
+        at = first_rfse_divergence((o["us"], o["vs"]), get(k))
+        if at is None:
+            full += 1
+            continue
+        cert = orc.rfse_divergence_certificate(s, lab, 0.8, 0.5, at, get(k))
+        assert cert["strict"] or cert["bounded"], (k, cert)
+        ties.append((k, cert))
+    print("identical", full, "certified ties", ties)
+
 
 
 @pytest.mark.parametrize("seed", range(_SEEDS or 4))
