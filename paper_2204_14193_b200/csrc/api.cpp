@@ -114,7 +114,7 @@ struct fse_plan {
   double *W64 = nullptr, *w64 = nullptr, *w00 = nullptr, *tmp = nullptr;
   // f64 path workspace
   int chunk = 0;
-  double *windows = nullptr, *recon = nullptr, *cs = nullptr, *es = nullptr;
+  double *cs = nullptr, *es = nullptr;
   int64_t *us = nullptr, *vs = nullptr;
   int32_t *status = nullptr;
   int32_t *selfs = nullptr, *counts = nullptr, *tallies = nullptr;  // generic rFSE outputs
@@ -457,8 +457,6 @@ int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int 
     // generic per-window path (fp64, or sizes the fused kernel does not cover)
     p->chunk = std::max(1, std::min(n_blocks, F <= 64 ? 2048 : 296));
     const size_t C = p->chunk, It = std::max(iterations, 1);
-    CK(p->alloc(&p->windows, C * FF));
-    CK(p->alloc(&p->recon, C * FF));
     CK(p->alloc(&p->us, C * It));
     CK(p->alloc(&p->vs, C * It));
     CK(p->alloc(&p->cs, C * It * 2));
@@ -565,20 +563,21 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
   const int F = p->F, B = p->B;
   for (int c0 = 0; c0 < p->n_blocks; c0 += p->chunk) {
     const int n = std::min(p->chunk, p->n_blocks - c0);
-    CK(fse::launch_gather_windows(frames, dtype, pitch, frame_stride, p->H, p->W,
-                                  p->blocks + (size_t)3 * c0, n, F, B, p->windows, st));
     fse::GenArgs a{};
     a.count = n; a.M = F; a.N = F; a.iterations = p->iterations; a.precision = p->precision;
     a.algorithm = p->algorithm; a.stop_tally = p->algorithm ? p->stop_tally : 0;
     a.selfs = p->selfs; a.counts = p->counts; a.tallies = p->tallies;
-    a.rho = p->rho; a.gamma = p->gamma; a.signal = p->windows; a.labels = p->labels;
+    a.rho = p->rho; a.gamma = p->gamma; a.signal = nullptr; a.labels = p->labels;
     a.labels_stride = (long long)F * F; a.label_index = p->block_class + c0;
-    a.recon = p->recon; a.model = nullptr; a.us = p->us; a.vs = p->vs; a.cs = p->cs; a.es = p->es;
+    a.wtab = p->w64;  // the class weights (class_setup_kernel, same formula)
+    a.recon = nullptr; a.model = nullptr; a.us = p->us; a.vs = p->vs; a.cs = p->cs; a.es = p->es;
+    const size_t esz = tile_dtype == 0 ? 1 : tile_dtype == 1 ? 4 : 8;
+    // image mode: windows cut from the frames and tiles written by the kernel
+    a.frames = frames; a.dtype = dtype; a.pitch = pitch; a.frame_stride = frame_stride;
+    a.H = p->H; a.W = p->W; a.B = B; a.blocks = p->blocks + (size_t)3 * c0;
+    a.tiles = (char *)tiles + (size_t)c0 * B * B * esz; a.tile_dtype = tile_dtype;
     a.status = p->status;
     CK(fse::launch_generic_extrapolate(a, p->gen_ws, st));
-    const size_t esz = tile_dtype == 0 ? 1 : tile_dtype == 1 ? 4 : 8;
-    CK(fse::launch_extract_tiles(p->recon, n, F, B, (char *)tiles + (size_t)c0 * B * B * esz,
-                                 tile_dtype, st));
     if (trace_uv) {  // trace: f64 entries for fp64 plans, f32 otherwise
       const size_t It = (size_t)p->iterations, tsz = p->precision == FSE_PREC_F64 ? 8 : 4;
       CK(fse::launch_pack_trace(p->us, p->vs, p->cs, p->es, p->algorithm ? p->counts : nullptr, n,

@@ -316,6 +316,98 @@ FSE_DEV void pick_bin(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p, i
   }
 }
 
+#ifndef FSE_GROUPMAX32
+#define FSE_GROUPMAX32 FSE_GROUPMAX
+#endif
+#ifndef FSE_GROUPMAX64
+#define FSE_GROUPMAX64 FSE_GROUPMAX
+#endif
+#ifndef FSE_GROUPMAX128
+#define FSE_GROUPMAX128 FSE_GROUPMAX
+#endif
+#ifndef FSE_GROUPMAX
+// first-max tracking per group of GM bin pairs: the group's maximum by a
+// three-input max tree (2 GM values, ~GM ops), then one compare + two
+// selects against the running maximum -- ~1.75 ALU ops per pair at GM = 4
+// instead of 5 for a per-pair tracker.  The exact first bin inside the
+// winning group is resolved after the warp maximum is known, by the lanes
+// holding it only (bitwise the same |R|^2 ops as the scan).  0 = per pair.
+#define FSE_GROUPMAX 0
+#endif
+
+// |R|^2 of the SoA pair p (the scan's exact instruction sequence)
+template <int NP> FSE_DEV float2 mag2(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p) {
+  float2 mg = __fmul2_rn(Rre[p], Rre[p]);
+  return __ffma2_rn(Rim[p], Rim[p], mg);
+}
+
+// maximum of the 2 GM |R|^2 values of a group (exact: returns one input)
+template <int GM> FSE_DEV float group_max(const float (&v)[2 * GM]) {
+  if constexpr (GM == 4) {
+    return fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmaxf(v[6], v[7]));
+  } else if constexpr (GM == 2) {
+    return fmaxf(fmax3(v[0], v[1], v[2]), v[3]);
+  } else {
+    float t = v[0];
+#pragma unroll
+    for (int i = 1; i < 2 * GM; ++i) t = fmaxf(t, v[i]);
+    return t;
+  }
+}
+
+// copy group G0's GM SoA pairs out of the spectrum registers
+template <int GM, int G0, int NP>
+FSE_DEV void group_copy(const float2 (&Rre)[NP], const float2 (&Rim)[NP], float2 (&gr)[GM],
+                        float2 (&gi)[GM]) {
+#pragma unroll
+  for (int q = 0; q < GM; ++q) {
+    gr[q] = Rre[G0 * GM + q];
+    gi[q] = Rim[G0 * GM + q];
+  }
+}
+
+#define FSE_RG(G0)                                                 \
+  case G0:                                                        \
+    if constexpr (G0 < NG) group_copy<GM, G0, NP>(Rre, Rim, gr, gi); \
+    break;
+
+// The first (pair, member) of group g whose |R|^2 equals target, and its
+// value.  g must be warp-uniform (a uniform jump, like pick_bin); |R|^2 is
+// recomputed with the scan's exact instruction sequence.
+template <int NP, int GM>
+FSE_DEV void resolve_group(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int g, float target,
+                           int &pp, int &mm, float &re, float &im) {
+  constexpr int NG = NP / GM;
+  static_assert(NG * GM == NP && NG <= 16, "groups tile the pairs");
+  float2 gr[GM], gi[GM];
+  if constexpr (NG <= 4) {
+    switch (g) { FSE_RG(0) FSE_RG(1) FSE_RG(2) FSE_RG(3) default: __builtin_unreachable(); }
+  } else if constexpr (NG <= 8) {
+    switch (g) {
+      FSE_RG(0) FSE_RG(1) FSE_RG(2) FSE_RG(3) FSE_RG(4) FSE_RG(5) FSE_RG(6) FSE_RG(7)
+      default: __builtin_unreachable();
+    }
+  } else {
+    switch (g) {
+      FSE_RG(0) FSE_RG(1) FSE_RG(2) FSE_RG(3) FSE_RG(4) FSE_RG(5) FSE_RG(6) FSE_RG(7)
+      FSE_RG(8) FSE_RG(9) FSE_RG(10) FSE_RG(11) FSE_RG(12) FSE_RG(13) FSE_RG(14) FSE_RG(15)
+      default: __builtin_unreachable();
+    }
+  }
+  // scan backwards so the first match in (pair, member) order is kept
+  pp = g * GM;
+  mm = 0;
+  re = gr[0].x;
+  im = gi[0].x;
+#pragma unroll
+  for (int q = GM - 1; q >= 0; --q) {
+    const float2 mg = __ffma2_rn(gi[q], gi[q], __fmul2_rn(gr[q], gr[q]));
+    if (mg.y == target) { pp = g * GM + q; mm = 1; re = gr[q].y; im = gi[q].y; }
+    if (mg.x == target) { pp = g * GM + q; mm = 0; re = gr[q].x; im = gi[q].x; }
+  }
+}
+#undef FSE_RG
+
 // ------------------------------------------------ radix-8 register FFT
 FSE_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 FSE_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
@@ -779,6 +871,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 #define FSE_PACKKEY 0
 #endif
       constexpr bool PK = FSE_PACKKEY && !G::PLANAR && CH == 1;
+      constexpr int GM = PK ? 0 : F == 32 ? FSE_GROUPMAX32 : F == 64 ? FSE_GROUPMAX64 : FSE_GROUPMAX128;
+      static_assert(GM == 0 || (CH == 1 && G::NP % GM == 0), "group tracker: one chain, whole groups");
+      float gv[GM > 0 ? 2 * GM : 2];  // the current group's |R|^2 values
+      int bg = 0;                     // GM: the thread's first group holding its maximum
       unsigned bkey = 0u;  // PK: truncated |R|^2 bits | (NP-1-p) << 1 | member a
       // (the mask laundered through a shuffle stays a register operand, so
       // clear-and-insert is one LOP3 with the rank as its immediate)
@@ -827,6 +923,13 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
             const unsigned ka = (__float_as_uint(mg.x) & kmask) | (unsigned)(((G::NP - 1 - p) << 1) | 1);
             const unsigned kb = (__float_as_uint(mg.y) & kmask) | (unsigned)((G::NP - 1 - p) << 1);
             bkey = max(bkey, max(ka, kb));
+          } else if constexpr (GM > 0) {
+            gv[2 * (p % GM)] = mg.x;
+            gv[2 * (p % GM) + 1] = mg.y;
+            if (p % GM == GM - 1) {
+              const float t = group_max<GM>(gv);
+              if (t > bst[0]) { bst[0] = t; bg = p / GM; }
+            }
           } else {
             first_max(bst[ch], bps[ch], bxs[ch], mg, p);
           }
@@ -852,7 +955,16 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           float2 mg = fmul2(Rre[p], Rre[p]);
           mg = ffma2(Rim[p], Rim[p], mg);
           const int ch = p / (G::NP / CH);
-          first_max(bst[ch], bps[ch], bxs[ch], mg, p);
+          if constexpr (GM > 0) {
+            gv[2 * (p % GM)] = mg.x;
+            gv[2 * (p % GM) + 1] = mg.y;
+            if (p % GM == GM - 1) {
+              const float t = group_max<GM>(gv);
+              if (t > bst[0]) { bst[0] = t; bg = p / GM; }
+            }
+          } else {
+            first_max(bst[ch], bps[ch], bxs[ch], mg, p);
+          }
         }
       }
       float best = bst[0], bx = bxs[0];
@@ -866,15 +978,44 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
                            : bin_index<F>(w, lane, bp, bx >= best ? 0 : 1);
       const unsigned key = PK ? (bkey & kmask) : __float_as_uint(best);  // best >= 0: monotone as unsigned
       const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
-      const unsigned widx = __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
       int pw, mw, ow;
+      float are, aim;
+      if constexpr (GM > 0) {
+        // Lanes holding the warp maximum, one at a time (usually one; a
+        // conjugate-mirror tie can give two): broadcast the lane's group, all
+        // lanes run the (then uniform) resolution on their own registers, and
+        // the lane's first bin equal to the maximum and its value are read
+        // back; the smallest row-major index wins the warp.
+        unsigned cand = __ballot_sync(0xffffffffu, key == wmax);
+        const float wbest = __uint_as_float(wmax);
+        unsigned widx = 0xffffffffu;
+        are = 0.f;
+        aim = 0.f;
+        do {
+          const int L = __ffs(cand) - 1;
+          cand &= cand - 1;
+          const int gL = __shfl_sync(0xffffffffu, bg, L);
+          int pp, mm;
+          float re = 0.f, im = 0.f;
+          resolve_group<G::NP, GM>(Rre, Rim, gL, wbest, pp, mm, re, im);
+          const int pm = __shfl_sync(0xffffffffu, (pp << 1) | mm, L);
+          const unsigned idx = (unsigned)bin_index<F>(w, L, pm >> 1, pm & 1);
+          re = __shfl_sync(0xffffffffu, re, L);
+          im = __shfl_sync(0xffffffffu, im, L);
+          if (idx < widx) { widx = idx; are = re; aim = im; }
+        } while (cand);
+        gidx = widx;
+        (void)pw; (void)mw; (void)ow;
+      } else {
+      const unsigned widx = __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
       decode_bin<F>((int)widx, w, pw, mw, ow);
       FSE_CHECK(pw >= 0 && pw < G::NP && ow >= 0 && ow < 32);
-      float are, aim;
       pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
       are = __shfl_sync(0xffffffffu, are, ow);
       aim = __shfl_sync(0xffffffffu, aim, ow);
       gidx = widx;
+      }
+      const unsigned widx = gidx;
 #if FSE_DIAG & 1
       if (false) {
 #else

@@ -21,6 +21,7 @@
 #include <float.h>
 #include <limits.h>
 #include <math_constants.h>
+#include <stdio.h>
 
 #include "common.cuh"
 #include "dft.cuh"
@@ -29,6 +30,24 @@
 namespace fse {
 
 constexpr int kGenThreads = 512;
+constexpr size_t kCandBytes = 2 * (kGenThreads / 32) * sizeof(double4);  // cfse_iterate_reg slots
+
+// block-wide maximum of v (every thread gets it)
+__device__ double block_max(double v, double *red) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  v = red[0];
+  __syncthreads();
+  return v;
+}
 
 // max |x[i]| over the samples with lab[i] == keep (all when lab is null)
 __device__ double block_max_abs(const double *x, int n, double *red, const int8_t *lab = nullptr,
@@ -192,24 +211,61 @@ __device__ void cfse_iterate(Cplx<T> *R, const Cplx<T> *W, int M, int N, T gamma
 // cfse_iterate with the residual spectrum in registers (windows of up to
 // kGenThreads * BPT bins: every size up to 64 x 64): thread t owns bins
 // t + kGenThreads j, j < BPT, in the same increasing order as the shared-
-// memory loop, so per-thread first maxima, the block reduction and every
-// IEEE op are identical (bit-exact); only W' is read from shared memory.
-// The winner's residual value travels with the reduction, so one barrier
-// per iteration publishes (value, index).
-template <typename T>
-__device__ void argmax_combine_v(T &v, int &i, T &re, T &im, T v2, int i2, T re2, T im2) {
-  if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; re = re2; im = im2; }
+// memory loop, so per-thread first maxima and every IEEE op are identical
+// (bit-exact); only W' is read from shared memory.  The block argmax is
+// latency-lean: a non-negative |R|^2 orders like its bit pattern, so a warp
+// finds its (value, first index) with two or three REDUX ops; the owning
+// lane publishes (value, index, R) to a double-buffered candidate slot; after
+// one barrier every warp merges the 16 candidates the same way and reads the
+// winner's residual with two shuffles.  Same total order as cfse.py:68-79
+// (larger |R|^2, then smaller row-major index).
+template <typename T> struct Key;
+template <> struct Key<double> {
+  static FSE_DEV unsigned hi(double v) { return (unsigned)__double2hiint(v); }
+  static FSE_DEV unsigned lo(double v) { return (unsigned)__double2loint(v); }
+};
+template <> struct Key<float> {
+  static FSE_DEV unsigned hi(float v) { return __float_as_uint(v); }
+  static FSE_DEV unsigned lo(float) { return 0u; }
+};
+
+// first maximum over the warp of (v >= 0, idx) for lanes with `valid`;
+// returns the winning index (0xffffffff when no lane is valid)
+template <typename T> FSE_DEV unsigned warp_first_max(T v, unsigned idx, bool valid) {
+  const unsigned h = valid ? Key<T>::hi(v) : 0u;
+  const unsigned l = valid ? Key<T>::lo(v) : 0u;
+  const unsigned wh = __reduce_max_sync(0xffffffffu, h);
+  unsigned wl = 0u;
+  if (sizeof(T) == 8) wl = __reduce_max_sync(0xffffffffu, h == wh ? l : 0u);
+  return __reduce_min_sync(0xffffffffu, valid && h == wh && l == wl ? idx : 0xffffffffu);
+}
+
+// one vector load of a complex value (16 B for double: LDS.128, not two LDS.64)
+FSE_DEV Cplx<double> load_cplx(const Cplx<double> *p) {
+  const double2 v = *(const double2 *)p;
+  return {v.x, v.y};
+}
+FSE_DEV Cplx<float> load_cplx(const Cplx<float> *p) {
+  const float2 v = *(const float2 *)p;
+  return {v.x, v.y};
+}
+
+// floor(i / n) for 0 <= i < 2^24, n >= 1 (float reciprocal + one correction)
+FSE_DEV int div_small(int i, int n, float rn) {
+  int q = __float2int_rz((float)i * rn);
+  q -= q * n > i;
+  q += (q + 1) * n <= i;
+  return q;
 }
 
 template <typename T, int BPT>
 __device__ void cfse_iterate_reg(const Cplx<T> *R0, const Cplx<T> *W, int M, int N, T gamma,
                                  T inv_w00, int iterations, double e0, int64_t *us, int64_t *vs,
-                                 double *cs, double *es, double *red) {
+                                 double *cs, double *es, double4 *cand) {
   typedef Ieee<T> F;
-  static_assert(kGenThreads / 32 * 2 * sizeof(double2) <= 64 * sizeof(double), "winner slots");
-  const int MN = M * N, tid = threadIdx.x;
-  // the warp winners: (value re, im) and (|R|^2, index), 16 warps
-  double2 *wa = (double2 *)red, *wb = wa + kGenThreads / 32;
+  constexpr int NW = kGenThreads / 32;
+  const int MN = M * N, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const float rn = 1.0f / (float)N;
   const T damp = F::mul(gamma, F::sub((T)2.0, gamma));
   T e = (T)e0;
   Cplx<T> R[BPT];
@@ -227,33 +283,28 @@ __device__ void cfse_iterate_reg(const Cplx<T> *R0, const Cplx<T> *W, int M, int
       if (m2 > best) { best = m2; bi = i; bre = R[j].re; bim = R[j].im; }
     }
   }
-  const int w = tid >> 5, lane = tid & 31;
   for (int it = 0; it < iterations; ++it) {
-    for (int o = 16; o; o >>= 1) {
-      const T v2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      const T r2 = __shfl_xor_sync(0xffffffffu, bre, o), m2 = __shfl_xor_sync(0xffffffffu, bim, o);
-      argmax_combine_v(best, bi, bre, bim, v2, i2, r2, m2);
-    }
-    if (lane == 0) {
-      wa[w] = make_double2((double)bre, (double)bim);
-      wb[w] = make_double2((double)best, __longlong_as_double((long long)bi));
-    }
+    double4 *slot = cand + (it & 1) * NW;
+    const bool have = best >= (T)0;
+    const unsigned widx = warp_first_max<T>(best, (unsigned)bi, have);
+    if (have && (unsigned)bi == widx)
+      slot[w] = make_double4((double)best, __longlong_as_double((long long)bi), (double)bre, (double)bim);
+    if (lane == 0 && widx == 0xffffffffu)
+      slot[w] = make_double4(-1.0, __longlong_as_double(-1ll), 0.0, 0.0);
     __syncthreads();
-    // every thread merges the 16 warp winners with the same total order
-    // (larger |R|^2, then smaller index)
-    T bv = (T)wb[0].x, ar = (T)wa[0].x, ai = (T)wa[0].y;
-    int bidx = (int)__double_as_longlong(wb[0].y);
-#pragma unroll 4
-    for (int q = 1; q < kGenThreads / 32; ++q) {
-      const double2 ca = wa[q], cb = wb[q];
-      argmax_combine_v(bv, bidx, ar, ai, (T)cb.x, (int)__double_as_longlong(cb.y), (T)ca.x, (T)ca.y);
-    }
-    const int idx = bidx;
-    const int u = idx / N, v = idx - u * N;
+    const double4 c4 = lane < NW ? slot[lane] : make_double4(-1.0, __longlong_as_double(-1ll), 0.0, 0.0);
+    const unsigned cidx = (unsigned)__double_as_longlong(c4.y);
+    const unsigned gidx = warp_first_max<T>((T)c4.x, cidx, c4.x >= 0.0);
+    const int ow = __ffs(__ballot_sync(0xffffffffu, lane < NW && cidx == gidx)) - 1;
+    const T ar = (T)__shfl_sync(0xffffffffu, c4.z, ow);
+    const T ai = (T)__shfl_sync(0xffffffffu, c4.w, ow);
+    const int idx = (int)gidx;
+    const int u = div_small(idx, N, rn), v = idx - u * N;
+    // c = gamma * rw_uv * inv_w00 (cfse.py:85): (gamma*a)*inv_w00
     const T cr = F::mul(F::mul(gamma, ar), inv_w00);
     const T ci = F::mul(F::mul(gamma, ai), inv_w00);
     if (tid == 0) {
+      // e -= damp * |rw_uv|^2 * inv_w00 (cfse.py:101)
       T m2 = F::add(F::mul(ar, ar), F::mul(ai, ai));
       e = F::sub(e, F::mul(F::mul(damp, m2), inv_w00));
       us[it] = u;
@@ -263,6 +314,7 @@ __device__ void cfse_iterate_reg(const Cplx<T> *R0, const Cplx<T> *W, int M, int
       es[it] = (double)e;
     }
     if (it + 1 == iterations) break;
+    // residual update (cfse.py:91-99) fused with the next pass's scan
     best = (T)-1.0;
     bi = 0;
 #pragma unroll
@@ -272,7 +324,7 @@ __device__ void cfse_iterate_reg(const Cplx<T> *R0, const Cplx<T> *W, int M, int
         int ks = kk[j] - u, ls = ll[j] - v;
         if (ks < 0) ks += M;
         if (ls < 0) ls += N;
-        const Cplx<T> wv = W[ks * N + ls];
+        const Cplx<T> wv = load_cplx(W + ks * N + ls);
         Cplx<T> x = R[j];
         T pr = F::sub(F::mul(cr, wv.re), F::mul(ci, wv.im));
         T pi = F::add(F::mul(cr, wv.im), F::mul(ci, wv.re));
@@ -283,7 +335,95 @@ __device__ void cfse_iterate_reg(const Cplx<T> *R0, const Cplx<T> *W, int M, int
         if (m2 > best) { best = m2; bi = i; bre = x.re; bim = x.im; }
       }
     }
-    __syncthreads();  // winner slots reuse
+    // no trailing barrier: the candidate slots are double-buffered
+  }
+  __syncthreads();
+}
+
+// cfse_iterate_reg for windows that tile the CTA exactly (MN = 512 BPT,
+// N | 512, M and N powers of two: every BASELINE size up to 64 x 64).
+// Thread t owns bins t + 512 j: column l = t mod N for every j, rows
+// k0 + (512/N) j.  W' comes from a row-extended table Wx = [W; W] (2M rows,
+// built here in the caller's free buffer `wx`), so the shifted bins of a
+// thread are one base address plus immediate strides -- no per-bin index
+// arithmetic or wrap, no per-bin bounds branch.  Same per-thread scan order,
+// IEEE ops and block reduction as cfse_iterate_reg (bit-identical results).
+template <typename T, int BPT>
+__device__ void cfse_iterate_tile(const Cplx<T> *R0, const Cplx<T> *W, Cplx<T> *wx, int M, int N, T gamma,
+                                  T inv_w00, int iterations, double e0, int64_t *us, int64_t *vs,
+                                  double *cs, double *es, double4 *cand) {
+  typedef Ieee<T> F;
+  constexpr int NW = kGenThreads / 32;
+  const int MN = M * N, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int logN = __ffs(N) - 1;
+  const T damp = F::mul(gamma, F::sub((T)2.0, gamma));
+  T e = (T)e0;
+  Cplx<T> R[BPT];
+  T best = (T)-1.0, bre = (T)0.0, bim = (T)0.0;
+  int bi = 0;
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {  // pass 0: load + scan
+    const int i = tid + kGenThreads * j;
+    R[j] = R0[i];
+    T m2 = F::add(F::mul(R[j].re, R[j].re), F::mul(R[j].im, R[j].im));
+    if (m2 > best) { best = m2; bi = i; bre = R[j].re; bim = R[j].im; }
+  }
+  __syncthreads();  // R0 may alias wx
+  for (int i = tid; i < 2 * MN; i += kGenThreads) {
+    const Cplx<T> x = W[i & (MN - 1)];
+    wx[i] = x;
+  }
+  __syncthreads();
+  const int k0 = tid >> logN, l0 = tid & (N - 1);
+  for (int it = 0; it < iterations; ++it) {
+    double4 *slot = cand + (it & 1) * NW;
+    const unsigned widx = warp_first_max<T>(best, (unsigned)bi, true);
+    if ((unsigned)bi == widx)
+      slot[w] = make_double4((double)best, __longlong_as_double((long long)bi), (double)bre, (double)bim);
+    __syncthreads();
+    const double4 c4 = lane < NW ? slot[lane] : make_double4(-1.0, __longlong_as_double(-1ll), 0.0, 0.0);
+    const unsigned cidx = (unsigned)__double_as_longlong(c4.y);
+    const unsigned gidx = warp_first_max<T>((T)c4.x, cidx, c4.x >= 0.0);
+    const int ow = __ffs(__ballot_sync(0xffffffffu, lane < NW && cidx == gidx)) - 1;
+    const T ar = (T)__shfl_sync(0xffffffffu, c4.z, ow);
+    const T ai = (T)__shfl_sync(0xffffffffu, c4.w, ow);
+    const int u = (int)gidx >> logN, v = (int)gidx & (N - 1);
+    // c = gamma * rw_uv * inv_w00 (cfse.py:85): (gamma*a)*inv_w00
+    const T cr = F::mul(F::mul(gamma, ar), inv_w00);
+    const T ci = F::mul(F::mul(gamma, ai), inv_w00);
+    if (tid == 0) {
+      // e -= damp * |rw_uv|^2 * inv_w00 (cfse.py:101)
+      T m2 = F::add(F::mul(ar, ar), F::mul(ai, ai));
+      e = F::sub(e, F::mul(F::mul(damp, m2), inv_w00));
+      us[it] = u;
+      vs[it] = v;
+      cs[2 * it] = (double)cr;
+      cs[2 * it + 1] = (double)ci;
+      es[it] = (double)e;
+    }
+    if (it + 1 == iterations) break;
+    // residual update (cfse.py:91-99) fused with the next pass's scan:
+    // bin j of this thread reads Wx[((k0 - u) mod M + (512/N) j) N + (l0 - v) mod N]
+    const Cplx<T> *wp = wx + ((((k0 - u) & (M - 1)) << logN) + ((l0 - v) & (N - 1)));
+    best = (T)-1.0;
+    bi = 0;
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const Cplx<T> wv = load_cplx(wp + kGenThreads * j);
+      Cplx<T> x = R[j];
+      T pr = F::sub(F::mul(cr, wv.re), F::mul(ci, wv.im));
+      T pi = F::add(F::mul(cr, wv.im), F::mul(ci, wv.re));
+      x.re = F::sub(x.re, pr);
+      x.im = F::sub(x.im, pi);
+      R[j] = x;
+      T m2 = F::add(F::mul(x.re, x.re), F::mul(x.im, x.im));
+      const bool gt = m2 > best;
+      best = gt ? m2 : best;
+      bi = gt ? tid + kGenThreads * j : bi;
+      bre = gt ? x.re : bre;
+      bim = gt ? x.im : bim;
+    }
+    // no trailing barrier: the candidate slots are double-buffered
   }
   __syncthreads();
 }
@@ -412,7 +552,8 @@ struct GenLayout {
 static GenLayout gen_layout(int M, int N, int precision) {
   GenLayout L{};
   size_t MN = (size_t)M * N;
-  size_t fixed = (size_t)(M + N) * sizeof(double2) * 2 + 64 * sizeof(double) + 64 * sizeof(int) + 64;
+  size_t fixed = (size_t)(M + N) * sizeof(double2) * 2 + 64 * sizeof(double) + 64 * sizeof(int) + 64 +
+                 kCandBytes;
   fixed = (fixed + 255) & ~(size_t)255;
   size_t big = 2 * MN * sizeof(double2);
   if (precision == 1) big += 2 * MN * sizeof(float2);
@@ -442,7 +583,26 @@ size_t generic_workspace_bytes(int count, int M, int N, int precision) {
   return L.ws_per_window * (size_t)count;
 }
 
-template <typename T, int ALG>
+// FSE_GDIAG=k diagnostic builds: return after setup phase k (timing only);
+// FSE_GCLK: thread 0 of window 0 prints the clock at every phase boundary
+#ifdef FSE_GDIAG
+#define FSE_GSTOP(k) \
+  if ((k) == FSE_GDIAG) return
+#elif defined(FSE_GCLK)
+#define FSE_GSTOP(k)                                                        \
+  do {                                                                      \
+    if (threadIdx.x == 0) gclk[(k)] = clock64() - gclk0;                    \
+    if ((k) == 7 && threadIdx.x == 0 && blockIdx.x == 0)                    \
+      for (int q = 0; q < 8; ++q) printf("phase %d clock %lld\n", q, gclk[q]); \
+  } while (0)
+#else
+#define FSE_GSTOP(k) ((void)0)
+#endif
+
+// SMEM: the window's work arrays live in shared memory (L.smem); a separate
+// instantiation so every access to them compiles to LDS/STS rather than
+// generic loads
+template <typename T, int ALG, bool SMEM>
 __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, GenLayout L,
                                                                    char *workspace) {
   extern __shared__ __align__(16) char smem[];
@@ -455,15 +615,56 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
   double *red = (double *)(twNp + N);
   int *redi = (int *)(red + 64);
   double4 *bcast = (double4 *)(redi + 64);
-  size_t fixed = (size_t)(M + N) * sizeof(double2) * 2 + 64 * sizeof(double) + 64 * sizeof(int) + 64;
+  double4 *cand = (double4 *)((char *)bcast + 64);  // 2 x 16 warp candidates
+  size_t fixed = (size_t)(M + N) * sizeof(double2) * 2 + 64 * sizeof(double) + 64 * sizeof(int) + 64 +
+                 kCandBytes;
   fixed = (fixed + 255) & ~(size_t)255;
-  char *region = L.smem ? smem + fixed : workspace + (size_t)win * L.ws_per_window;
+  char *region = SMEM ? smem + fixed : workspace + (size_t)win * L.ws_per_window;
   double2 *A = (double2 *)(region + L.off_A);
   double2 *Bf = (double2 *)(region + L.off_B);
   Cplx<T> *R = (Cplx<T> *)(region + L.off_R);
   Cplx<T> *Wt = (Cplx<T> *)(region + L.off_W);
 
-  const double *s = a.signal + (size_t)win * MN;
+#ifdef FSE_GCLK
+  const long long gclk0 = clock64();
+  __shared__ long long gclk[8];
+#endif
+  const bool img = a.frames != nullptr;
+  const double *s = img ? nullptr : a.signal + (size_t)win * MN;
+  int wt = 0, wl = 0, off = 0;
+  size_t fbase = 0;
+  if (img) {
+    off = (M - a.B) / 2;
+    fbase = (size_t)a.blocks[3 * win] * (size_t)a.frame_stride;
+    wt = a.blocks[3 * win + 1] - off;
+    wl = a.blocks[3 * win + 2] - off;
+  }
+  // window sample i (image mode: from the frame, 0 outside it)
+  auto sval = [&](int i) -> double {
+    if (!img) return s[i];
+    const int m = i / N, n = i - m * N, y = wt + m, x = wl + n;
+    if (y < 0 || y >= a.H || x < 0 || x >= a.W) return 0.0;
+    const size_t o = fbase + (size_t)y * a.pitch + x;
+    return a.dtype == 0 ? (double)((const uint8_t *)a.frames)[o]
+                        : a.dtype == 1 ? (double)((const float *)a.frames)[o] : ((const double *)a.frames)[o];
+  };
+  // output of window sample i: recon (every sample) or, in image mode, the
+  // loss tile (u8: clamp + round half even)
+  auto put = [&](int i, double v, bool loss) {
+    if (!img) {
+      a.recon[(size_t)win * MN + i] = loss ? v : s[i];
+      return;
+    }
+    if (!loss) return;
+    const int m = i / N, n = i - m * N;
+    const size_t o = (size_t)win * a.B * a.B + (size_t)(m - off) * a.B + (n - off);
+    if (a.tile_dtype == 0)
+      ((uint8_t *)a.tiles)[o] = (uint8_t)__double2int_rn(fmin(fmax(v, 0.0), 255.0));
+    else if (a.tile_dtype == 1)
+      ((float *)a.tiles)[o] = (float)v;
+    else
+      ((double *)a.tiles)[o] = v;
+  };
   const int8_t *lab =
       a.labels + (size_t)(a.label_index ? a.label_index[win] : win) * a.labels_stride;
   int64_t *us = a.us + (size_t)win * a.iterations;
@@ -479,13 +680,18 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     twN[j] = twiddle(j, N, -1);
     twNp[j] = twiddle(j, N, +1);
   }
+  FSE_GSTOP(0);
   // kappa = 2^-e with max|s| = f 2^e, f in [0.5, 1): balances the two real
   // signals packed into one complex DFT; scaling by a power of two is exact.
   // Only support samples enter the transforms: loss / padding samples have
   // w = 0, so this equals the reference for finite input, and a non-finite
   // value in the lost block (common for decoded frames) cannot leak into
   // the window through 0 * NaN.
-  double smax = block_max_abs(s, MN, red, lab, kSupport);
+  double smax = 0.0;
+  for (int i = threadIdx.x; i < MN; i += blockDim.x)
+    if (lab[i] == kSupport) smax = fmax(smax, fabs(sval(i)));
+  smax = block_max(smax, red);
+  FSE_GSTOP(1);
   int ex = 0;
   if (smax > 0.0) frexp(smax, &ex);
   const double kappa = ldexp(1.0, -ex), inv_kappa = ldexp(1.0, ex);
@@ -493,26 +699,40 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
   for (int i = threadIdx.x; i < MN; i += blockDim.x) {
     int m = i / N, n = i - m * N;
     const bool sup = lab[i] == kSupport;
-    double w = sup ? weight_at(m, n, M, N, a.rho) : 0.0;
-    const double si = sup ? s[i] : 0.0;
+    double w = !sup ? 0.0 : a.wtab ? a.wtab[(size_t)a.label_index[win] * a.labels_stride + i]
+                                   : weight_at(m, n, M, N, a.rho);
+    const double si = sup ? sval(i) : 0.0;
     double sw = si * w;
     A[i] = make_double2(w, sw * kappa);
     e0p += w * si * si;  // np.sum(w * s * s), cfse.py:51
   }
   const double e0 = block_sum(e0p, red);  // includes barrier
-  dft_rows(A, Bf, M, N, twN);
-  __syncthreads();
-  dft_cols(Bf, A, M, N, twM);
-  __syncthreads();
+  FSE_GSTOP(2);
+  // power-of-two sizes: in-place radix-2 FFTs (log-depth, a few us for 64 x
+  // 64); other sizes: the separable direct DFT
+  const int logM = ilog2_pow2(M), logN = ilog2_pow2(N);
+  const bool pow2 = logM >= 0 && logN >= 0;
+  if (M == 64 && N == 64 && blockDim.x == 512) {  // register radix-8 x 8, Bf as exchange
+    fft64_axis(A, Bf, false, false, twN);
+    fft64_axis(A, Bf, true, false, twM);
+  } else if (pow2) {
+    if (N > 1) fft_axis(A, logN, logM, 1, N, twN);
+    if (M > 1) fft_axis(A, logM, logN, N, 1, twM);
+  } else {
+    dft_rows(A, Bf, M, N, twN);
+    __syncthreads();
+    dft_cols(Bf, A, M, N, twM);
+    __syncthreads();
+  }
   unpack_two_real(A, Bf, M, N, inv_kappa);  // Bf = W, A = R_w
+  FSE_GSTOP(3);
   __syncthreads();
   const double w00 = Bf[0].x;
   // rejected windows still write their output: the input outside the loss,
   // NaN on it (never stale memory).  Plans reject these geometries at
   // creation; the per-window status reports them to the direct API.
-  double *rec_out = a.recon + (size_t)win * MN;
   if (w00 <= 1e-12 * (double)M * (double)N) {  // cfse.py:47-48
-    for (int i = threadIdx.x; i < MN; i += blockDim.x) rec_out[i] = lab[i] == kLoss ? CUDART_NAN : s[i];
+    for (int i = threadIdx.x; i < MN; i += blockDim.x) put(i, CUDART_NAN, lab[i] == kLoss);
     if (threadIdx.x == 0) a.status[win] = 1;
     return;
   }
@@ -527,7 +747,7 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
       if (D <= 1e-9 * w00 * w00) bad = 1;
     }
     if (__syncthreads_or(bad)) {
-      for (int i = threadIdx.x; i < MN; i += blockDim.x) rec_out[i] = lab[i] == kLoss ? CUDART_NAN : s[i];
+      for (int i = threadIdx.x; i < MN; i += blockDim.x) put(i, CUDART_NAN, lab[i] == kLoss);
       if (threadIdx.x == 0) a.status[win] = 2;
       return;
     }
@@ -542,8 +762,21 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     __syncthreads();
   }
   int n_it = a.iterations;
-  if (ALG == 0 && MN <= kGenThreads * 8) {
-    cfse_iterate_reg<T, 8>(R, Wt, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, red);
+  FSE_GSTOP(4);
+  // the exactly-tiling register loop: MN = 512 BPT, N | 512, powers of two;
+  // its row-extended W' table goes to the (then free) A buffer, which holds
+  // 2 MN complex values for either precision (A + Bf for fp64)
+  const int tile_bpt = pow2 && (MN % kGenThreads) == 0 && N <= kGenThreads ? MN / kGenThreads : 0;
+  if (ALG == 0 && (tile_bpt == 8 || tile_bpt == 4 || tile_bpt == 2)) {
+    Cplx<T> *wx = (Cplx<T> *)A;
+    if (tile_bpt == 8)
+      cfse_iterate_tile<T, 8>(R, Wt, wx, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, cand);
+    else if (tile_bpt == 4)
+      cfse_iterate_tile<T, 4>(R, Wt, wx, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, cand);
+    else
+      cfse_iterate_tile<T, 2>(R, Wt, wx, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, cand);
+  } else if (ALG == 0 && MN <= kGenThreads * 8) {
+    cfse_iterate_reg<T, 8>(R, Wt, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, cand);
   } else if (ALG == 0) {
     cfse_iterate<T>(R, Wt, M, N, (T)a.gamma, (T)inv_w00, a.iterations, e0, us, vs, cs, es, nullptr,
                     (T *)red, redi, bcast);
@@ -553,12 +786,53 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
                     redi, bcast);
     n_it = a.counts[win];
   }
-  // synthesis g = sum c e^{+2 pi i (u m/M + v n/N)} and write-back
-  double *rec = a.recon + (size_t)win * MN;
+  // synthesis g = idft2(G) (cfse.py:126): G[u,v] += MN c in iteration order
+  // (cfse.py:88; rFSE also adds MN conj(c) at the mirror bin, rfse.py:128-
+  // 145), then inverse FFTs and 1/(MN) -- or, for other sizes, the direct
+  // sum g = sum c e^{+2 pi i (u m/M + v n/N)} over the trace
   double *model = a.model ? a.model + (size_t)win * 2 * MN : nullptr;
+  if (pow2) {
+    FSE_GSTOP(5);
+    __syncthreads();  // trace (global, written by thread 0) visible; A free
+    for (int i = threadIdx.x; i < MN; i += blockDim.x) A[i] = make_double2(0.0, 0.0);
+    __syncthreads();
+    const double dmn = (double)MN;
+    for (int it = 0; it < n_it; ++it) {  // each bin accumulated by one thread, in order
+      const int idx = (int)us[it] * N + (int)vs[it];
+      const double cr = cs[2 * it], ci = cs[2 * it + 1];
+      if ((idx & (kGenThreads - 1)) == (int)threadIdx.x) {
+        A[idx].x = __dadd_rn(A[idx].x, __dmul_rn(dmn, cr));
+        A[idx].y = __dadd_rn(A[idx].y, __dmul_rn(dmn, ci));
+      }
+      if (ALG == 1 && !a.selfs[(size_t)win * a.iterations + it]) {
+        const int mi = ((M - (int)us[it]) & (M - 1)) * N + ((N - (int)vs[it]) & (N - 1));
+        if ((mi & (kGenThreads - 1)) == (int)threadIdx.x) {
+          A[mi].x = __dadd_rn(A[mi].x, __dmul_rn(dmn, cr));
+          A[mi].y = __dadd_rn(A[mi].y, __dmul_rn(dmn, -ci));
+        }
+      }
+    }
+    __syncthreads();
+    if (M == 64 && N == 64 && blockDim.x == 512) {  // W no longer needed: Bf is the exchange
+      fft64_axis(A, Bf, false, true, twN);
+      fft64_axis(A, Bf, true, true, twM);
+    } else {
+      if (N > 1) fft_axis(A, logN, logM, 1, N, twNp);
+      if (M > 1) fft_axis(A, logM, logN, N, 1, twMp);
+    }
+    FSE_GSTOP(6);
+    const double sc = 1.0 / dmn;
+    for (int i = threadIdx.x; i < MN; i += blockDim.x) {
+      const double gr = A[i].x * sc;
+      if (model) { model[2 * i] = gr; model[2 * i + 1] = A[i].y * sc; }
+      put(i, gr, lab[i] == kLoss);
+    }
+    FSE_GSTOP(7);
+    return;
+  }
   for (int i = threadIdx.x; i < MN; i += blockDim.x) {
     const bool loss = lab[i] == kLoss;
-    if (!loss && !model) { rec[i] = s[i]; continue; }
+    if (!loss && !model) { put(i, 0.0, false); continue; }
     int m = i / N, n = i - m * N;
     double gr = 0.0, gi = 0.0;
     for (int it = 0; it < n_it; ++it) {
@@ -576,7 +850,7 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
       }
     }
     if (model) { model[2 * i] = gr; model[2 * i + 1] = gi; }
-    rec[i] = loss ? gr : s[i];
+    put(i, gr, loss);
   }
 }
 
@@ -591,10 +865,17 @@ cudaError_t launch_generic_extrapolate(const GenArgs &a, void *workspace, cudaSt
     kern<<<a.count, kGenThreads, L.smem_bytes, st>>>(a, L, (char *)workspace);
     return cudaGetLastError();
   };
-  if (a.algorithm == 1)
-    e = a.precision == 1 ? launch(extrapolate_kernel<float, 1>) : launch(extrapolate_kernel<double, 1>);
-  else
-    e = a.precision == 1 ? launch(extrapolate_kernel<float, 0>) : launch(extrapolate_kernel<double, 0>);
+  if (L.smem) {
+    if (a.algorithm == 1)
+      e = a.precision == 1 ? launch(extrapolate_kernel<float, 1, true>) : launch(extrapolate_kernel<double, 1, true>);
+    else
+      e = a.precision == 1 ? launch(extrapolate_kernel<float, 0, true>) : launch(extrapolate_kernel<double, 0, true>);
+  } else {
+    if (a.algorithm == 1)
+      e = a.precision == 1 ? launch(extrapolate_kernel<float, 1, false>) : launch(extrapolate_kernel<double, 1, false>);
+    else
+      e = a.precision == 1 ? launch(extrapolate_kernel<float, 0, false>) : launch(extrapolate_kernel<double, 0, false>);
+  }
   return e;
 }
 
@@ -748,58 +1029,6 @@ cudaError_t launch_update_residual_f64(int M, int N, double *R, const double *W,
 }
 
 // ---------------------------------------------------- image-level helpers
-__global__ void gather_windows_kernel(const void *frames, int dtype, long long pitch,
-                                      long long frame_stride, int H, int W, const int32_t *blocks,
-                                      int F, int B, double *windows) {
-  const int b = blockIdx.x;
-  const int f = blocks[3 * b], top = blocks[3 * b + 1], left = blocks[3 * b + 2];
-  const int off = (F - B) / 2, wt = top - off, wl = left - off;
-  double *dst = windows + (size_t)b * F * F;
-  for (int i = threadIdx.x; i < F * F; i += blockDim.x) {
-    int m = i / F, n = i - m * F, y = wt + m, x = wl + n;
-    double v = 0.0;
-    if (y >= 0 && y < H && x >= 0 && x < W) {
-      size_t idx = (size_t)f * frame_stride + (size_t)y * pitch + x;
-      v = dtype == 0 ? (double)((const uint8_t *)frames)[idx]
-                     : dtype == 1 ? (double)((const float *)frames)[idx] : ((const double *)frames)[idx];
-    }
-    dst[i] = v;
-  }
-}
-
-cudaError_t launch_gather_windows(const void *frames, int dtype, long long pitch,
-                                  long long frame_stride, int H, int W, const int32_t *blocks,
-                                  int n, int F, int B, double *windows, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  gather_windows_kernel<<<n, 256, 0, s>>>(frames, dtype, pitch, frame_stride, H, W, blocks, F, B,
-                                          windows);
-  return cudaGetLastError();
-}
-
-__global__ void extract_tiles_kernel(const double *recon, int F, int B, void *tiles, int tile_dtype) {
-  const int b = blockIdx.x, off = (F - B) / 2;
-  for (int i = threadIdx.x; i < B * B; i += blockDim.x) {
-    int r = i / B, c = i - r * B;
-    double v = recon[(size_t)b * F * F + (size_t)(off + r) * F + off + c];
-    size_t o = (size_t)b * B * B + i;
-    if (tile_dtype == 0) {
-      double cl = fmin(fmax(v, 0.0), 255.0);
-      ((uint8_t *)tiles)[o] = (uint8_t)__double2int_rn(cl);
-    } else if (tile_dtype == 1) {
-      ((float *)tiles)[o] = (float)v;
-    } else {
-      ((double *)tiles)[o] = v;
-    }
-  }
-}
-
-cudaError_t launch_extract_tiles(const double *recon, int n, int F, int B, void *tiles,
-                                 int tile_dtype, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  extract_tiles_kernel<<<n, 256, 0, s>>>(recon, F, B, tiles, tile_dtype);
-  return cudaGetLastError();
-}
-
 __global__ void pack_trace_kernel(const int64_t *us, const int64_t *vs, const double *cs,
                                   const double *es, const int32_t *counts, int n, int It,
                                   int32_t *uv, void *c, void *e, int c64) {

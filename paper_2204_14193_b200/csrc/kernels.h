@@ -16,6 +16,16 @@ struct GenArgs {
   const int8_t *labels;
   long long labels_stride;
   const int32_t *label_index;  // optional: window i uses labels + label_index[i]*labels_stride
+  const double *wtab;          // optional (with label_index): per-class weights w, labels_stride apart
+  // image mode (plans): frames != null -- window i is cut from the frames
+  // around blocks[3 i..] (frame, top, left) instead of read from `signal`,
+  // and the B x B loss tile goes straight to `tiles` (tile_dtype) instead of
+  // `recon`
+  const void *frames;
+  int dtype, H, W, B, tile_dtype;
+  long long pitch, frame_stride;
+  const int32_t *blocks;
+  void *tiles;
   double *recon, *model;
   int64_t *us, *vs;
   double *cs, *es;
@@ -106,13 +116,6 @@ cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensor
 size_t fast_stage_bytes(int F);
 
 // ------------------------------------------------------------- image f64
-// Gather F x F windows (f64, zero outside the image) for a list of blocks.
-cudaError_t launch_gather_windows(const void *frames, int dtype, long long pitch,
-                                  long long frame_stride, int H, int W, const int32_t *blocks,
-                                  int n, int F, int B, double *windows, cudaStream_t s);
-// Copy the B x B loss tiles out of reconstructed windows into tiles.
-cudaError_t launch_extract_tiles(const double *recon, int n, int F, int B, void *tiles,
-                                 int tile_dtype, cudaStream_t s);
 // Pack the per-window trace (us, vs int64; cs re/im f64; es f64; `counts`
 // executed iterations per window or null = all) into the plan trace layout:
 // uv int32 (n, It, 2), c (n, It, 2) and e (n, It) as f64 (c64 != 0) or f32;
