@@ -529,3 +529,26 @@ def test_concealer_tile_paths_agree(fse):
     import torch
     out = torch.zeros((len(blocks), 16, 16), dtype=torch.uint8).pin_memory()
     assert np.array_equal(a.run(h, out=out), ta)
+
+
+@pytest.mark.parametrize("F,B,border", [(64, 8, 8), (32, 16, 4), (16, 4, 4)])
+def test_fp32_generic_geometries(fse, F, B, border):
+    """fp32 plans outside the fused kernel's geometry (B != F/4) run the
+    per-window kernel in fp32 (the exactly-tiling register loop for 64 x 64
+    and 32 x 32, the general loop otherwise): fp32 gate against the oracle."""
+    from paper_2204_14193_b200.synth import field
+    img = field(160, 224, seed=F + B).astype(np.float32)
+    rng = np.random.default_rng(F)
+    n = 24
+    blocks = np.stack([np.zeros(n, np.int64), rng.integers(0, 160 - B + 1, n),
+                       rng.integers(0, 224 - B + 1, n)], 1).astype(np.int32)
+    plan = fse.ConcealPlan(blocks, 160, 224, fse.Geometry(B, border, F), rho_hat=0.8, gamma=0.5,
+                           iterations=80, precision="fp32")
+    assert plan.info["fast_path"] == 0
+    import torch
+    tiles, tr = plan.run(torch.from_numpy(img).cuda(), tile_dtype="f32", trace=True)
+    uv = tr["uv"].cpu().numpy(); c = tr["c"].cpu().numpy()
+    get = lambda k: (uv[k, :, 0].astype(np.int64), uv[k, :, 1].astype(np.int64), c[k, :, 0] + 1j * c[k, :, 1])
+    st = fp32_gate(img, blocks, tiles.cpu().numpy(), get, F, B, border, 0.8, 0.5, 80,
+                   truth=_truth(img, blocks, B), log=f"fp32_generic_{F}_{B}")
+    print(F, B, {k: v for k, v in st.items() if k != "outliers"})
