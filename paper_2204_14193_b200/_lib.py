@@ -123,5 +123,28 @@ def stream_ptr(stream=None) -> int:
     return int(s.cuda_stream)
 
 
+_STAGING = __import__("threading").local()
+
+
+def pinned_staging(nbytes: int, keep: int = 4):
+    """A pinned host byte buffer of `nbytes` for the calling thread (the
+    per-window latency paths copy every output back in one DMA).  Buffers
+    live in thread-local storage, so they are released with their thread,
+    and at most `keep` sizes are cached per thread (least recently used
+    dropped)."""
+    import torch
+
+    cache = getattr(_STAGING, "bufs", None)
+    if cache is None:
+        cache = _STAGING.bufs = {}
+    buf = cache.pop(nbytes, None)
+    if buf is None:
+        buf = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    cache[nbytes] = buf  # most recent last
+    while len(cache) > keep:
+        cache.pop(next(iter(cache)))
+    return buf
+
+
 def ptr(t) -> int | None:
     return None if t is None else int(t.data_ptr())

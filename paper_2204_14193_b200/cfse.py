@@ -87,9 +87,6 @@ def extrapolate_cfse_batch(signals, labels, config: FseConfig, *, want_model: bo
                 es=es[:, :it], status=status)
 
 
-_PINNED: dict = {}  # per-size pinned staging buffers of extrapolate_cfse (one per thread use at a time)
-
-
 def extrapolate_cfse(signal, mask: AreaMask, config: FseConfig) -> ExtrapolationResult:
     """Run the complex-valued extrapolation and replace the loss samples
     (cfse.py:110-142).  Support and padding samples of the output equal the
@@ -117,10 +114,7 @@ def extrapolate_cfse(signal, mask: AreaMask, config: FseConfig) -> Extrapolation
     _lib.check(_lib.lib().fse_extrapolate(
         1, M, N, _prec(config), sd.data_ptr(), lab.data_ptr(), 0, float(config.rho_hat),
         float(config.gamma), it, p[0], p[1], p[2], p[3], p[4], p[5], p[6], _lib.stream_ptr(None)))
-    key = (int(offs[-1]), __import__("threading").get_ident())
-    host = _PINNED.get(key)
-    if host is None:
-        host = _PINNED[key] = torch.empty(int(offs[-1]), dtype=torch.uint8).pin_memory()
+    host = _lib.pinned_staging(int(offs[-1]))
     host.copy_(dev)  # synchronous: waits for the kernel
     raw = host.numpy()
 

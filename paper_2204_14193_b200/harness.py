@@ -60,7 +60,7 @@ class ConcealPlan:
     """
 
     def __init__(self, blocks, H: int, W: int, geometry: Geometry = Geometry(), *,
-                 rho_hat: float = 0.8, gamma: float = 0.5, iterations: int = 100,
+                 rho_hat: float = 0.8, gamma: float = 0.2, iterations: int = 100,
                  precision: str = "fp32", algorithm: str = "cfse", basis_target=None,
                  stream=None):
         torch = _lib.require_cuda()
@@ -160,7 +160,7 @@ class Concealer:
     """
 
     def __init__(self, blocks, n_frames: int, H: int, W: int, geometry: Geometry = Geometry(), *,
-                 rho_hat: float = 0.8, gamma: float = 0.5, iterations: int = 100,
+                 rho_hat: float = 0.8, gamma: float = 0.2, iterations: int = 100,
                  precision: str = "fp32", chunk_frames=None, frame_dtype=np.uint8,
                  tile_dtype: str = "u8", algorithm: str = "cfse", basis_target=None,
                  tile_path: str = "host"):
@@ -275,7 +275,7 @@ class Concealer:
         return res
 
 
-def conceal_frames(frames, blocks, geometry: Geometry = Geometry(), *, rho_hat=0.8, gamma=0.5,
+def conceal_frames(frames, blocks, geometry: Geometry = Geometry(), *, rho_hat=0.8, gamma=0.2,
                    iterations=100, precision="fp32", tile_dtype="u8", algorithm="cfse",
                    basis_target=None):
     """One-shot form: device or host frames, returns tiles (same side)."""

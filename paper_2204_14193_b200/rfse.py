@@ -73,11 +73,10 @@ def extrapolate_rfse(signal, mask: AreaMask, config: FseConfig) -> Extrapolation
     flags, basis_count = tally (2 per pair, 1 per self-conjugate atom)."""
     s = _as_signal(signal)
     _validate(s, mask, config)
-    if s.ndim != 2:
-        return _from_batch(s, mask, config)
+    if s.ndim != 2:  # rfse.py -> cfse.py:36-40 via _prepare: the signal must be fft_dims
+        raise ConfigError(f"signal shape {s.shape} does not match configured FFT dims {config.fft_dims}")
     # latency path (as cfse.extrapolate_cfse): every output in one device
     # buffer, one copy to pinned host memory
-    import threading
     torch = _lib.require_cuda()
     M, N = s.shape
     MN = M * N
@@ -93,10 +92,7 @@ def extrapolate_rfse(signal, mask: AreaMask, config: FseConfig) -> Extrapolation
     _lib.check(_lib.lib().fse_extrapolate_rfse(
         1, M, N, _prec(config), sd.data_ptr(), lab.data_ptr(), 0, float(config.rho_hat),
         float(config.gamma), max_iters, stop, *p, _lib.stream_ptr(None)))
-    key = (int(offs[-1]), threading.get_ident())
-    host = _PINNED.get(key)
-    if host is None:
-        host = _PINNED[key] = torch.empty(int(offs[-1]), dtype=torch.uint8).pin_memory()
+    host = _lib.pinned_staging(int(offs[-1]))
     host.copy_(dev)  # synchronous: waits for the kernel
     raw = host.numpy()
 
@@ -120,22 +116,6 @@ def extrapolate_rfse(signal, mask: AreaMask, config: FseConfig) -> Extrapolation
                                model=part(1, np.complex128, MN).reshape(M, N), trace=trace,
                                basis_count=int(part(8, np.int32, 1)[0]))
 
-
-_PINNED: dict = {}
-
-
-def _from_batch(s, mask, config):
-    out = extrapolate_rfse_batch(s[None], mask.labels, config, want_model=True)
-    cnt = int(out["counts"][0])
-    us, vs = out["us"][0, :cnt].cpu().numpy(), out["vs"][0, :cnt].cpu().numpy()
-    cs, es = out["cs"][0, :cnt].cpu().numpy(), out["es"][0, :cnt].cpu().numpy()
-    sf = out["selfs"][0, :cnt].cpu().numpy()
-    trace = [IterationRecord(index=i, frequency=(int(us[i]), int(vs[i])), coefficient=complex(cs[i]),
-                             residual_energy=float(es[i]), self_conjugate=bool(sf[i]))
-             for i in range(cnt)]
-    return ExtrapolationResult(reconstructed=out["reconstructed"][0].cpu().numpy(),
-                               model=out["model"][0].cpu().numpy(), trace=trace,
-                               basis_count=int(out["tallies"][0]))
 
 
 class RfsePlan:

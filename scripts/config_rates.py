@@ -48,7 +48,7 @@ fr1 = torch.from_numpy(img1).to(dev)
 s = dev_time(lambda: p64.run(fr1, tile_dtype="f64"))
 mask = fse.build_mask((64, 64), (24, 24, 16, 16), 16)
 win = img1[96:160, 96:160].copy()
-cfg = fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=100)
+cfg = fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=100, gamma=0.5)
 fse.extrapolate_cfse(win, mask, cfg)
 ts = []
 for _ in range(20):
@@ -62,9 +62,9 @@ print(json.dumps({"config": "1 (fp64, one block)", "blocks": 1, "F": 64, "iterat
 img2 = torch.from_numpy(field(512, 512, seed=2).astype(np.float32)).to(dev)
 tl = grid_blocks(512, 512, 16)
 b2 = np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
-report("2 (fp32, 256 blocks)", fse.ConcealPlan(b2, 512, 512, fse.Geometry(16, 16, 64), iterations=100),
+report("2 (fp32, 256 blocks)", fse.ConcealPlan(b2, 512, 512, fse.Geometry(16, 16, 64), iterations=100, gamma=0.5),
        img2, len(b2), 64, 100, tile_dtype="f32")
-p2d = fse.ConcealPlan(b2, 512, 512, fse.Geometry(16, 16, 64), iterations=100, precision="fp64")
+p2d = fse.ConcealPlan(b2, 512, 512, fse.Geometry(16, 16, 64), iterations=100, precision="fp64", gamma=0.5)
 report("2 (fp64 reference-arithmetic plan, 256 blocks)", p2d, img2.double(), len(b2), 64, 100,
        tile_dtype="f64", reps=5)
 
@@ -72,7 +72,7 @@ report("2 (fp64 reference-arithmetic plan, 256 blocks)", p2d, img2.double(), len
 fr3 = field_torch(64, 1080, 1920, seed=3, device=dev, edges=True)
 b3 = fse.frames_pattern(64, 1080, 1920, 16, 0.10, seed=3)
 report("3 (u8, 64 x 1080p, 10% loss, I=200)",
-       fse.ConcealPlan(b3, 1080, 1920, fse.Geometry(16, 16, 64), iterations=200), fr3, len(b3), 64, 200,
+       fse.ConcealPlan(b3, 1080, 1920, fse.Geometry(16, 16, 64), iterations=200, gamma=0.5), fr3, len(b3), 64, 200,
        reps=5)
 del fr3
 
@@ -80,16 +80,16 @@ del fr3
 img4 = torch.from_numpy(field(512, 512, seed=4).astype(np.float32)).to(dev)
 tl = np.array([(16 * i, 16 * j) for i in range(32) for j in range(32)], np.int32)[::2][:500]
 b4a = np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
-report("4a (fp32, 500 x 8x8, F=32)", fse.ConcealPlan(b4a, 512, 512, fse.Geometry(8, 8, 32), iterations=100),
+report("4a (fp32, 500 x 8x8, F=32)", fse.ConcealPlan(b4a, 512, 512, fse.Geometry(8, 8, 32), iterations=100, gamma=0.5),
        img4, len(b4a), 32, 100, tile_dtype="f32")
 imgs = torch.from_numpy(np.stack([field(512, 512, seed=40 + k) for k in range(8)]).astype(np.float32)).to(dev)
 b4b = np.array([(f, 64 * i, 64 * j) for f in range(8) for i in range(8) for j in range(8)], np.int32)[:500]
 report("4b (fp32, 500 x 32x32, F=128)",
-       fse.ConcealPlan(b4b, 512, 512, fse.Geometry(32, 16, 128), iterations=100), imgs, len(b4b), 128, 100,
+       fse.ConcealPlan(b4b, 512, 512, fse.Geometry(32, 16, 128), iterations=100, gamma=0.5), imgs, len(b4b), 128, 100,
        tile_dtype="f32")
 
 # config 5: 256 x 4K u8 + edges, 5% loss (the bench workload)
 fr5 = field_torch(256, 2160, 3840, seed=5, device=dev, edges=True)
 b5 = fse.frames_pattern(256, 2160, 3840, 16, 0.05, seed=5)
-report("5 (u8, 256 x 4K, 5% loss)", fse.ConcealPlan(b5, 2160, 3840, fse.Geometry(16, 16, 64), iterations=100),
+report("5 (u8, 256 x 4K, 5% loss)", fse.ConcealPlan(b5, 2160, 3840, fse.Geometry(16, 16, 64), iterations=100, gamma=0.5),
        fr5, len(b5), 64, 100, reps=5)

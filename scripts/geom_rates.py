@@ -13,7 +13,7 @@ for F, B, border in ((32, 8, 8), (64, 16, 16), (128, 32, 16)):
     if only and F not in only:
         continue
     blocks = fse.frames_pattern(16, 2160, 3840, B, 0.05 if B < 32 else 0.04, seed=2)
-    plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(B, border, F), iterations=100)
+    plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(B, border, F), iterations=100, gamma=0.5)
     t = plan.run(frames); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()

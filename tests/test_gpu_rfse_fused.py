@@ -310,3 +310,17 @@ def test_fused_rfse_global_trace(fse, F):
     t64 = ref.run(fr, tile_dtype="f64")
     cert = _rfse_gate(fse, img, blocks, t32, tr32, t64, F, B, iters, iters + 100)
     print(F, "certified near-ties:", cert)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_rfse_plan_rejects_degenerate_pair_geometry(fse, precision):
+    """A 17 x 16 image with its one 16 x 16 block at the origin: the clipped
+    support is one row, every (k, 0) pair's Gram determinant vanishes
+    (rfse.py:47-55).  Every rFSE plan -- fp64 per-window as well as the fused
+    fp32 one -- raises ConfigError at creation (never stale tiles)."""
+    with pytest.raises(fse.ConfigError):
+        fse.ConcealPlan(np.array([[0, 0, 0]], np.int32), 17, 16, fse.Geometry(16, 16, 64),
+                        algorithm="rfse", precision=precision, iterations=10)
+    # the same geometry is fine for cFSE
+    fse.ConcealPlan(np.array([[0, 0, 0]], np.int32), 17, 16, fse.Geometry(16, 16, 64),
+                    precision=precision, iterations=10)

@@ -117,3 +117,39 @@ def test_synthetic_field_stats():
     assert abs(x.mean() - 128) < 1.5 and abs(x.std() - 40) < 1.5
     f = frame_u8(128, 256, 1)
     assert f.dtype == np.uint8 and f.shape == (128, 256)
+
+
+def test_rfse_rejects_a_3d_signal_like_the_reference():
+    """rfse.extrapolate_rfse on a (1, M, N) signal: ConfigError (the
+    reference's _prepare checks signal.shape == fft_dims), no CUDA needed."""
+    cfg = fse.FseConfig(fft_dims=(8, 8), algorithm="rfse")
+    mask = fse.build_mask((8, 8), (2, 2, 4, 4), 2)
+    with pytest.raises(fse.ConfigError):
+        fse.extrapolate_rfse(np.zeros((1, 8, 8)), mask, cfg)
+    with pytest.raises(fse.ConfigError):
+        fse.extrapolate_cfse(np.zeros((1, 8, 8)), mask, fse.FseConfig(fft_dims=(8, 8)))
+
+
+def test_pinned_staging_is_thread_local_and_bounded(monkeypatch):
+    """The latency paths' pinned staging buffers live per thread and at most
+    `keep` sizes are cached (no unbounded module-level cache)."""
+    import threading
+
+    class FakeT:
+        def __init__(self, n):
+            self.n = n
+
+        def pin_memory(self):
+            return self
+
+    import torch
+    monkeypatch.setattr(torch, "empty", lambda n, dtype=None: FakeT(n))
+    a = _lib.pinned_staging(100)
+    assert _lib.pinned_staging(100) is a
+    for n in range(200, 800, 100):
+        _lib.pinned_staging(n)
+    assert len(_lib._STAGING.bufs) == 4 and 100 not in _lib._STAGING.bufs
+    other = []
+    t = threading.Thread(target=lambda: other.append(_lib.pinned_staging(100)))
+    t.start(); t.join()
+    assert other[0] is not _lib._STAGING.bufs.get(100)
