@@ -189,6 +189,25 @@ int fse_plan_run(const fse_plan *plan, const void *frames, int dtype, long long 
                  long long frame_stride, int n_frames, void *tiles, int tile_dtype,
                  int32_t *trace_uv, void *trace_c, void *trace_e, void *stream);
 
+/* Spatial-domain brute-force matching pursuit (no FFT): the independent
+ * equivalence check of `fse selfcheck` (the spec's
+ * `oracle` module, which the reference package does not ship).  Every
+ * iteration projects the spatial residual onto every atom by direct
+ * summation (Eq. 9), selects by Eq. (10) with the row-major first-max rule,
+ * updates model and residual in the spatial domain (Eqs. 13, 14, 17).
+ * pair_mode = 1: the rFSE pair rule (rfse.py:37-167), basis_target as in
+ * fse_extrapolate_rfse.  M, N <= 32.  Device arrays: signal, labels (int8,
+ * labels_stride apart), recon (count x M x N), us / vs / cs (c128) / es /
+ * es_direct (the directly evaluated weighted residual energy) of count x
+ * iterations (x basis_target in pair mode), selfs / counts / tallies
+ * (int32, optional), status (int32: 0, 1 empty support, 2 degenerate pairs). */
+int fse_spatial_extrapolate(int count, int M, int N, const double *signal, const int8_t *labels,
+                            long long labels_stride, double rho, double gamma, int iterations,
+                            int pair_mode, int basis_target, double *recon, int64_t *us,
+                            int64_t *vs, double *cs, double *es, double *es_direct,
+                            int32_t *selfs, int32_t *counts, int32_t *tallies, int32_t *status,
+                            void *stream);
+
 /* Seeded isolated-loss pattern: random-sequential
  * selection on the B x B block grid of an H x W frame, rejecting blocks
  * 8-adjacent to an already chosen one, until `count` blocks are chosen or

@@ -63,6 +63,7 @@ _SIGS = {
     "fse_plan_destroy": ([P], I),
     "fse_plan_run": ([P, P, I, LL, LL, I, P, I, P, P, P, P], I),
     "fse_loss_pattern": ([I, I, I, I, ctypes.c_uint64, P], I),
+    "fse_spatial_extrapolate": ([I, I, I, P, P, LL, D, D, I, I, I, P, P, P, P, P, P, P, P, P, P, P], I),
 }
 
 

@@ -58,7 +58,9 @@ def parser():
     b.add_argument("--repetitions", type=int, default=5)
     b.add_argument("--report")
     _common(b)
-    sub.add_parser("selfcheck")
+    k = sub.add_parser("selfcheck")
+    k.add_argument("--seed", type=int, default=0)
+    k.add_argument("--instances", type=int, default=50)
     return ap
 
 
@@ -218,22 +220,30 @@ def cmd_bench(a):
     return 0
 
 
-def cmd_selfcheck(_a):
-    """Internal consistency checks on the GPU (no CPU reference involved):
-    DFT round trip and Parseval, energy-decrease identity of the trace
-    against the directly evaluated weighted residual energy, scale
-    equivariance, support samples unchanged, fp32 vs fp64 agreement."""
+def cmd_selfcheck(a):
+    """the oracle-equivalence and energy-identity suites on
+    seeded random instances (selfcheck.run: the production frequency-domain
+    GPU path against the spatial-domain brute force, csrc/spatial.cu, for
+    cFSE and rFSE), then internal consistency checks: DFT round trip and
+    Parseval, energy identity of a 64 x 64 trace, scale equivariance,
+    support samples unchanged, fp32 vs fp64 agreement.  PASS/FAIL per
+    invariant; exit 0 only if every one passes."""
     from . import cfse, spectral
+    from . import selfcheck as sc
     from .types import FseConfig
     from .weighting import build_mask, build_weight
 
-    rng = np.random.default_rng(0)
+    seed = getattr(a, "seed", 0)
+    rng = np.random.default_rng(seed)
     ok = True
 
-    def check(name, cond):
+    def check(name, cond, detail=""):
         nonlocal ok
-        print(f"{'PASS' if cond else 'FAIL'} {name}")
+        print(f"{'PASS' if cond else 'FAIL'} {name}" + (f"  [{detail}]" if detail != "" else ""))
         ok &= bool(cond)
+
+    for name, passed, detail in sc.run(seed=seed, n=getattr(a, "instances", 50)):
+        check(name, passed, detail)
 
     x = rng.standard_normal((16, 16)) + 1j * rng.standard_normal((16, 16))
     X = spectral.dft2(x)

@@ -590,6 +590,33 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
   return FSE_OK;
 }
 
+// ------------------------------------------------ spatial self-check
+
+int fse_spatial_extrapolate(int count, int M, int N, const double *signal, const int8_t *labels,
+                            long long labels_stride, double rho, double gamma, int iterations,
+                            int pair_mode, int basis_target, double *recon, int64_t *us,
+                            int64_t *vs, double *cs, double *es, double *es_direct,
+                            int32_t *selfs, int32_t *counts, int32_t *tallies, int32_t *status,
+                            void *stream) {
+  if (int r = check_dims(M, N)) return r;
+  if (int r = check_rho_gamma(rho, gamma)) return r;
+  if (M > 32 || N > 32)
+    return fail(FSE_ERR_UNSUPPORTED, "spatial brute force is O(I M^2 N^2): M, N <= 32 (got %dx%d)", M, N);
+  if (iterations < 0) return fail(FSE_ERR_CONFIG, "iterations must be >= 0");
+  if (count <= 0) return FSE_OK;
+  if (!signal || !labels || !recon || !status || !us || !vs || !cs || !es || !es_direct)
+    return fail(FSE_ERR_VALUE, "null pointer");
+  fse::SpatialArgs a{};
+  a.count = count; a.M = M; a.N = N; a.pair_mode = pair_mode ? 1 : 0;
+  a.iterations = pair_mode && basis_target >= 0 ? basis_target : iterations;
+  a.stop_tally = pair_mode && basis_target >= 0 ? basis_target : 2 * iterations + 1;
+  a.rho = rho; a.gamma = gamma; a.signal = signal; a.labels = labels; a.labels_stride = labels_stride;
+  a.recon = recon; a.us = us; a.vs = vs; a.cs = cs; a.es = es; a.es_direct = es_direct;
+  a.selfs = selfs; a.counts = counts; a.tallies = tallies; a.status = status;
+  CK(fse::launch_spatial(a, S(stream)));
+  return FSE_OK;
+}
+
 // --------------------------------------------------- loss pattern (host)
 
 static inline uint64_t splitmix64(uint64_t &x) {

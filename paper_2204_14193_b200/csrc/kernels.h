@@ -124,4 +124,21 @@ cudaError_t launch_pack_trace(const int64_t *us, const int64_t *vs, const double
                               const double *es, const int32_t *counts, int n, int It,
                               int32_t *uv, void *c, void *e, int c64, cudaStream_t s);
 
+// ------------------------------------------------------------- spatial
+// Spatial-domain brute-force matching pursuit (spatial.cu): the package's
+// independent self-check.  M, N <= 32.
+struct SpatialArgs {
+  int count, M, N, iterations, pair_mode, stop_tally;
+  double rho, gamma;
+  const double *signal;   // count x M x N
+  const int8_t *labels;   // labels_stride apart
+  long long labels_stride;
+  double *recon;          // count x M x N
+  int64_t *us, *vs;       // count x iterations
+  double *cs, *es, *es_direct;
+  int32_t *selfs, *counts, *tallies, *status;  // selfs / counts / tallies optional
+};
+size_t spatial_smem_bytes(int M, int N);
+cudaError_t launch_spatial(const SpatialArgs &a, cudaStream_t s);
+
 }  // namespace fse

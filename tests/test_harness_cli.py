@@ -99,3 +99,50 @@ def test_cli_sweep_determinism_and_quality(tmp_path, cuda_ok):
                          "--precision", "fp32"]) == 0
         outs.append(open(out, "rb").read())
     assert outs[0] == outs[1]
+
+
+@pytest.mark.gpu
+def test_selfcheck_spatial_oracle_equivalence(capsys):
+    """`fse selfcheck`: the shipped GPU spatial brute force
+    agrees with the production path on the SPEC's seeded instances, and every
+    invariant passes (exit 0)."""
+    from paper_2204_14193_b200 import cli
+    assert cli.main(["selfcheck", "--instances", "50"]) == 0
+    out = capsys.readouterr().out
+    assert "FAIL" not in out and out.count("PASS") >= 12
+    print(out)
+
+
+@pytest.mark.gpu
+def test_spatial_kernel_matches_reference_goldens():
+    """The GPU spatial brute force against the reference's own outputs on
+    the small golden windows (tests/golden/small.npz, rfse.npz; M, N <= 16):
+    canonical selections, pixels within 1e-9."""
+    import numpy as np
+    import paper_2204_14193_b200 as fse
+    from paper_2204_14193_b200 import selfcheck as sc
+    from tests import _golden
+    n = 0
+    for c in _golden.load("small.npz") + _golden.load("rfse.npz"):
+        M, N = c["signal"].shape
+        if M > 32 or N > 32 or c["iterations"] == 0:
+            continue
+        pair = "selfs" in c
+        bt = c.get("basis_target", -1)
+        cfg = fse.FseConfig(rho_hat=c["rho"], gamma=c["gamma"], iterations=c["iterations"], fft_dims=(M, N),
+                            algorithm="rfse" if pair else "cfse", basis_target=None if bt < 0 else bt)
+        if pair and bt == 0:
+            continue
+        o = sc.spatial_extrapolate(c["signal"], fse.AreaMask(c["labels"]), cfg, pair_mode=pair)
+        if pair:
+            assert np.array_equal(o["us"], c["us"]) and np.array_equal(o["vs"], c["vs"]), c["name"]
+        else:
+            a = sc.canonical(o["us"], o["vs"], o["cs"], M, N)
+            b = sc.canonical(c["us"], c["vs"], c["cs"], M, N)
+            cut = np.nonzero(np.abs(b[2]) < 1e-10 * np.abs(b[2]).max())[0]  # residual at the fp64 floor
+            k = int(cut[0]) if cut.size else len(b[0])
+            assert np.array_equal(a[0][:k], b[0][:k]) and np.array_equal(a[1][:k], b[1][:k]), c["name"]
+        loss = c["labels"] == 2
+        np.testing.assert_allclose(o["reconstructed"][loss], c["recon_loss"], rtol=0, atol=1e-9)
+        n += 1
+    assert n >= 12
