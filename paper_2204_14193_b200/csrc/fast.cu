@@ -330,8 +330,11 @@ FSE_DEV void pick_bin(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p, i
 // three-input max tree (2 GM values, ~GM ops), then one compare + two
 // selects against the running maximum -- ~1.75 ALU ops per pair at GM = 4
 // instead of 5 for a per-pair tracker.  The exact first bin inside the
-// winning group is resolved after the warp maximum is known, by the lanes
-// holding it only (bitwise the same |R|^2 ops as the scan).  0 = per pair.
+// winning group is resolved after the warp maximum is known (bitwise the
+// same |R|^2 ops as the scan; scripts/ab_bitwise.py: identical tiles and
+// traces).  Measured slower at every size (config 5: 7.07 -> 6.29 M
+// blocks/s at GM = 4, 5.64 at GM = 8; F = 128: 1.20 -> 1.13 M): the longer
+// per-iteration tail costs more than the ALU ops it saves.  0 = per pair.
 #define FSE_GROUPMAX 0
 #endif
 
