@@ -48,7 +48,7 @@ fr1 = torch.from_numpy(img1).to(dev)
 s = dev_time(lambda: p64.run(fr1, tile_dtype="f64"))
 mask = fse.build_mask((64, 64), (24, 24, 16, 16), 16)
 win = img1[96:160, 96:160].copy()
-cfg = fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=100, gamma=0.5)
+cfg = fse.FseConfig(rho_hat=0.8, gamma=0.5, iterations=100)
 fse.extrapolate_cfse(win, mask, cfg)
 ts = []
 for _ in range(20):
