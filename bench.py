@@ -261,8 +261,13 @@ def run_reference(a, cfg, rank):
     t = time.perf_counter()
     orc.conceal_blocks(frames, blocks[:n1], *args, nthreads=1)
     single = n1 / (time.perf_counter() - t)
-    for _ in range(a.warmup):
+    # warm-up: the requested steps, and at least ~3 s of all-core work (a fresh
+    # box's first seconds of CPU time were measured 40 % slower)
+    t = time.perf_counter()
+    k = 0
+    while k < a.warmup or time.perf_counter() - t < 3.0:
         orc.conceal_blocks(frames, blocks, *args, nthreads=cores)
+        k += 1
     t = time.perf_counter()
     for _ in range(a.steps):
         orc.conceal_blocks(frames, blocks, *args, nthreads=cores)
