@@ -117,15 +117,17 @@ class ConcealPlan:
         device-to-host copy."""
         import torch
 
-        if not frames.is_cuda:
-            raise ValueError("ConcealPlan.run needs device frames; use Concealer for host frames")
+        if not (frames.is_cuda or frames.is_pinned()):
+            raise ValueError("ConcealPlan.run needs device frames or page-locked host frames "
+                             "(pageable host frames: use Concealer)")
         f3 = frames if frames.ndim == 3 else frames[None]
         if f3.shape[1] != self.H or f3.shape[2] != self.W or f3.stride(2) != 1:
             raise ValueError(f"frames {tuple(f3.shape)} do not match plan {self.H}x{self.W}")
         B = self.geometry.B
         tdt = {"u8": torch.uint8, "f32": torch.float32, "f64": torch.float64}[tile_dtype]
         if tiles is None:
-            tiles = torch.empty((self.n_blocks, B, B), dtype=tdt, device=f3.device)
+            tiles = torch.empty((self.n_blocks, B, B), dtype=tdt,
+                                device=f3.device if f3.is_cuda else torch.device("cuda", self.device))
         elif (tuple(tiles.shape) != (self.n_blocks, B, B) or tiles.dtype != tdt
               or not tiles.is_contiguous()):
             raise ValueError(f"tiles must be a contiguous {tdt} tensor of shape "

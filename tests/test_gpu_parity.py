@@ -552,3 +552,29 @@ def test_fp32_generic_geometries(fse, F, B, border):
     st = fp32_gate(img, blocks, tiles.cpu().numpy(), get, F, B, border, 0.8, 0.5, 80,
                    truth=_truth(img, blocks, B), log=f"fp32_generic_{F}_{B}")
     print(F, B, {k: v for k, v in st.items() if k != "outliers"})
+
+
+def test_frames_read_from_pinned_host_memory(fse):
+    """ConcealPlan.run on page-locked host frames: the kernel reads each
+    support window over the host link (TMA tile loads from mapped host
+    memory for u8, direct loads otherwise) -- tiles identical to the
+    device-resident run, for u8 (TMA and direct) and f32 frames."""
+    import os
+    import torch
+    from paper_2204_14193_b200.synth import field_torch
+    dev = field_torch(3, 270, 480, seed=12, device="cuda")
+    blocks = fse.frames_pattern(3, 270, 480, 16, 0.06, seed=12)
+    plan = fse.ConcealPlan(blocks, 270, 480, gamma=0.5, iterations=60)
+    ref = plan.run(dev, tile_dtype="f32").cpu()
+    host = dev.cpu().pin_memory()
+    for tma in ("1", "0"):
+        os.environ["FSE_TMA"] = tma
+        try:
+            got = plan.run(host, tile_dtype="f32")
+        finally:
+            del os.environ["FSE_TMA"]
+        assert torch.equal(got.cpu(), ref)
+    f32 = dev.float()
+    assert torch.equal(plan.run(f32.cpu().pin_memory(), tile_dtype="f32").cpu(), plan.run(f32, tile_dtype="f32").cpu())
+    with pytest.raises(ValueError):  # pageable host frames are refused
+        plan.run(dev.cpu())
