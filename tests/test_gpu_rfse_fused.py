@@ -324,3 +324,29 @@ def test_rfse_plan_rejects_degenerate_pair_geometry(fse, precision):
     # the same geometry is fine for cFSE
     fse.ConcealPlan(np.array([[0, 0, 0]], np.int32), 17, 16, fse.Geometry(16, 16, 64),
                     precision=precision, iterations=10)
+
+
+@pytest.mark.parametrize("F", [64, 32])
+def test_fused_rfse_on_a_config_frame(fse, F):
+    """Fused fp32 rFSE at scale against the C oracle's rFSE: F = 64 on the
+    bench's first 4K frame (1,620 blocks, basis_target 100), F = 32 on the
+    config-4a image (500 blocks of 8 x 8, 50 iterations)."""
+    from paper_2204_14193_b200.synth import field, field_torch
+    import torch
+    if F == 64:
+        frames = field_torch(1, 2160, 3840, seed=5 * 7919, device="cuda")
+        blocks = fse.frames_pattern(1, 2160, 3840, 16, 0.05, seed=5)
+        kw, iters, bt = dict(iterations=100, basis_target=100), 100, 100
+    else:
+        img = field(512, 512, seed=4).astype(np.float32)
+        frames = torch.from_numpy(img).cuda()[None]
+        tl = np.array([(16 * i, 16 * j) for i in range(32) for j in range(32)], np.int32)[::2][:500]
+        blocks = np.concatenate([np.zeros((len(tl), 1), np.int32), tl], 1)
+        kw, iters, bt = dict(iterations=50), 50, None
+    B = F // 4
+    plan = fse.ConcealPlan(blocks, frames.shape[1], frames.shape[2], fse.Geometry(B, B, F), rho_hat=0.8,
+                           gamma=0.5, algorithm="rfse", precision="fp32", **kw)
+    assert plan.info["fast_path"] == 1
+    t32, tr = plan.run(frames, tile_dtype="f32", trace=True)
+    st = _rfse_gate(fse, frames, blocks, t32, tr, None, F, B, iters, bt, log=f"rfse{F}_config_frame")
+    print(F, st)
