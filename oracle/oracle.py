@@ -549,30 +549,37 @@ def rfse_crit_of_coefficient(c, u, v, W, w00, gamma):
 
 
 def rfse_divergence_certificate(signal, labels, rho, gamma, upto: int, trace_fp32) -> dict:
-    """rFSE analogue of divergence_certificate: the fp64 oracle stepped to
-    `upto` (the fp32 run's first differing selection); `deficit` = relative
-    criterion gap between the fp64 pick and the fp32 pick, `err` = the fp32
-    run's measured criterion error (the largest |crit(c32) - crit(c64)| over
-    the shared selections, crit implied by the coefficient, and at the fp32
-    pick itself).  strict: deficit < 1e-6; bounded: gap <= 2 err."""
+    """rFSE analogue of divergence_certificate, in amplitude units: the fp64
+    oracle is stepped to `upto` (the fp32 run's first differing selection);
+    with q = sqrt(criterion) (the pair criterion is a quadratic form of the
+    residual, so q is linear in it, like |R_w| for cFSE):
+      deficit   (crit_top - crit_pick) / crit_top at the fp64 state,
+      gap_amp   q_top - q_pick,
+      err_amp   the fp32 run's measured error in the same units: the largest
+                |q(c32) - q(c64)| over the shared selections (q implied by
+                the coefficient, rfse_crit_of_coefficient) and at the fp32
+                pick itself.
+    strict: deficit < 1e-6; bounded: gap_amp <= 2 err_amp."""
     R, W, w00, pre = _rfse_state(signal, labels, rho, gamma, upto)
     us32, vs32, cs32 = (np.asarray(x) for x in trace_fp32[:3])
     crit = rfse_crit_map(R, W, w00)
     top = float(np.max(crit))
     pu, pv = int(us32[upto]), int(vs32[upto])
     pick = float(crit[pu, pv])
+    q = lambda x: float(np.sqrt(max(x, 0.0)))
     err = []
     if pre is not None:
         _, ous, ovs, ocs, _, _, _ = pre
         for k in range(upto):
             u, v = int(ous[k]), int(ovs[k])
-            err.append(abs(rfse_crit_of_coefficient(cs32[k], u, v, W, w00, gamma)
-                           - rfse_crit_of_coefficient(ocs[k], u, v, W, w00, gamma)))
-    err.append(abs(rfse_crit_of_coefficient(cs32[upto], pu, pv, W, w00, gamma) - pick))
-    gap = top - pick
-    deficit = gap / top if top > 0 else 0.0
-    return dict(at=int(upto), deficit=float(deficit), gap=float(gap), err=float(max(err)),
-                strict=bool(deficit < 1e-6), bounded=bool(gap <= 2.0 * max(err)))
+            err.append(abs(q(rfse_crit_of_coefficient(cs32[k], u, v, W, w00, gamma))
+                           - q(rfse_crit_of_coefficient(ocs[k], u, v, W, w00, gamma))))
+    err.append(abs(q(rfse_crit_of_coefficient(cs32[upto], pu, pv, W, w00, gamma)) - q(pick)))
+    err_amp = float(max(err))
+    gap_amp = q(top) - q(pick)
+    deficit = (top - pick) / top if top > 0 else 0.0
+    return dict(at=int(upto), deficit=float(deficit), gap_amp=gap_amp, err_amp=err_amp,
+                strict=bool(deficit < 1e-6), bounded=bool(gap_amp <= 2.0 * err_amp))
 
 
 def near_tie_gap(signal, labels, rho, gamma, upto: int) -> float:

@@ -100,10 +100,10 @@ def test_rfse_certificate_of_a_forced_second_best_pick():
         su, sv, p = mu, mv, p.conjugate()
     tr = (np.append(us, su), np.append(vs, sv), np.append(cs, gamma * p))
     cert = orc.rfse_divergence_certificate(s, lab, rho, gamma, k, tr)
-    gap = crit.ravel()[top] - crit[su, sv]
-    assert abs(cert["gap"] - gap) <= 1e-9 * crit.ravel()[top]
-    assert cert["err"] <= 1e-9 * crit.ravel()[top]
+    gap = np.sqrt(crit.ravel()[top]) - np.sqrt(crit[su, sv])
+    assert abs(cert["gap_amp"] - gap) <= 1e-9 * np.sqrt(crit.ravel()[top])
+    assert cert["err_amp"] <= 1e-9 * np.sqrt(crit.ravel()[top])
     assert not cert["bounded"]
     cs2 = tr[2].copy()
     cs2[k - 1] *= 1 + 1e-3
-    assert orc.rfse_divergence_certificate(s, lab, rho, gamma, k, (tr[0], tr[1], cs2))["err"] > 0
+    assert orc.rfse_divergence_certificate(s, lab, rho, gamma, k, (tr[0], tr[1], cs2))["err_amp"] > 0
