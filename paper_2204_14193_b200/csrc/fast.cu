@@ -700,21 +700,26 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
             v[fi][k] = make_float2(xe, xo);
           }
         } else {
+          // weights and pixels are loaded independently (in-bounds pixels
+          // unconditionally) so a cold window costs one memory round trip,
+          // not two dependent ones; samples off the support (w = 0, e.g. a
+          // NaN-filled lost block) are zeroed by a select, not multiplied
 #pragma unroll
           for (int k = 0; k < VPT; ++k) {
             const int n = t + Q * k, x = wl + n;
             float xe = 0.f, xo = 0.f;
             if (act && x >= 0 && x < a.W) {
               const float we = __ldg(wtab + (2 * j) * F + n), wo = __ldg(wtab + (2 * j + 1) * F + n);
-              if (we != 0.f && y0 >= 0 && y0 < a.H) {
-                const float s = load_px(a.frames, a.dtype, fbase + (size_t)y0 * a.pitch + x);
-                xe = s * we;
-                e0p += xe * s;
+              const bool ie = y0 >= 0 && y0 < a.H, io = y0 + 1 >= 0 && y0 + 1 < a.H;
+              const float se = ie ? load_px(a.frames, a.dtype, fbase + (size_t)y0 * a.pitch + x) : 0.f;
+              const float so = io ? load_px(a.frames, a.dtype, fbase + (size_t)(y0 + 1) * a.pitch + x) : 0.f;
+              if (we != 0.f) {
+                xe = se * we;
+                e0p += xe * se;
               }
-              if (wo != 0.f && y0 + 1 >= 0 && y0 + 1 < a.H) {
-                const float s = load_px(a.frames, a.dtype, fbase + (size_t)(y0 + 1) * a.pitch + x);
-                xo = s * wo;
-                e0p += xo * s;
+              if (wo != 0.f) {
+                xo = so * wo;
+                e0p += xo * so;
               }
             }
             v[fi][k] = make_float2(xe, xo);
@@ -859,7 +864,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 #ifndef FSE_CHAINS128
 #define FSE_CHAINS128 1
 #endif
-      constexpr int CH = F == 64 ? FSE_CHAINS64 : F == 128 ? FSE_CHAINS128 : 1;
+#ifndef FSE_CHAINS32
+#define FSE_CHAINS32 1
+#endif
+      constexpr int CH = F == 64 ? FSE_CHAINS64 : F == 128 ? FSE_CHAINS128 : FSE_CHAINS32;
       float bst[CH], bxs[CH];
       int bps[CH];
 #pragma unroll

@@ -375,12 +375,21 @@ __device__ void cfse_iterate_tile(const Cplx<T> *R0, const Cplx<T> *W, Cplx<T> *
   }
   __syncthreads();
   const int k0 = tid >> logN, l0 = tid & (N - 1);
+#ifdef FSE_GCLK
+  long long ck[6] = {0, 0, 0, 0, 0, 0}, cl = clock64();
+#define FSE_LCLK(j) do { const long long c2 = clock64(); ck[j] += c2 - cl; cl = c2; } while (0)
+#else
+#define FSE_LCLK(j) ((void)0)
+#endif
   for (int it = 0; it < iterations; ++it) {
     double4 *slot = cand + (it & 1) * NW;
     const unsigned widx = warp_first_max<T>(best, (unsigned)bi, true);
+    FSE_LCLK(0);
     if ((unsigned)bi == widx)
       slot[w] = make_double4((double)best, __longlong_as_double((long long)bi), (double)bre, (double)bim);
+    FSE_LCLK(1);
     __syncthreads();
+    FSE_LCLK(2);
     const double4 c4 = lane < NW ? slot[lane] : make_double4(-1.0, __longlong_as_double(-1ll), 0.0, 0.0);
     const unsigned cidx = (unsigned)__double_as_longlong(c4.y);
     const unsigned gidx = warp_first_max<T>((T)c4.x, cidx, c4.x >= 0.0);
@@ -391,6 +400,7 @@ __device__ void cfse_iterate_tile(const Cplx<T> *R0, const Cplx<T> *W, Cplx<T> *
     // c = gamma * rw_uv * inv_w00 (cfse.py:85): (gamma*a)*inv_w00
     const T cr = F::mul(F::mul(gamma, ar), inv_w00);
     const T ci = F::mul(F::mul(gamma, ai), inv_w00);
+    FSE_LCLK(3);
     if (tid == 0) {
       // e -= damp * |rw_uv|^2 * inv_w00 (cfse.py:101)
       T m2 = F::add(F::mul(ar, ar), F::mul(ai, ai));
@@ -423,8 +433,15 @@ __device__ void cfse_iterate_tile(const Cplx<T> *R0, const Cplx<T> *W, Cplx<T> *
       bre = gt ? x.re : bre;
       bim = gt ? x.im : bim;
     }
+    FSE_LCLK(4);
     // no trailing barrier: the candidate slots are double-buffered
   }
+#ifdef FSE_GCLK
+  if (tid == 0 && blockIdx.x == 0)
+    printf("iteration phases (thread 0, cycles/iter): warp argmax %lld, publish %lld, barrier %lld, merge+c %lld, update+scan %lld\n",
+           ck[0] / iterations, ck[1] / iterations, ck[2] / iterations, ck[3] / iterations, ck[4] / iterations);
+#endif
+#undef FSE_LCLK
   __syncthreads();
 }
 
