@@ -245,17 +245,17 @@ def run_reference(a, cfg, rank):
         return
     from oracle import oracle as orc
 
-    nf = 1
-    frames, gen_dev = reference_frames(cfg, a.config, 16)
-    blocks_all = orc.frames_pattern(16, cfg["H"], cfg["W"], cfg["B"], cfg["frac"], SEED if a.config == "5" else 3)
-    per_frame = len(blocks_all) // 16
+    nmax = min(16, cfg["frames"])
+    frames, gen_dev = reference_frames(cfg, a.config, nmax)
+    blocks_all = orc.frames_pattern(nmax, cfg["H"], cfg["W"], cfg["B"], cfg["frac"], SEED if a.config == "5" else 3)
+    per_frame = len(blocks_all) // nmax
     cores = len(os.sched_getaffinity(0))
     args = (cfg["B"], cfg["border"], cfg["F"], RHO, GAMMA, cfg["iters"])
     probe = blocks_all[: min(len(blocks_all), 4 * cores)]
     t = time.perf_counter()
     orc.conceal_blocks(frames, probe, *args, nthreads=cores)
     rate = len(probe) / max(time.perf_counter() - t, 1e-3)
-    nf = max(1, min(16, int(round(1.5 * rate / per_frame))))
+    nf = max(1, min(nmax, int(round(1.5 * rate / per_frame))))
     blocks = blocks_all[blocks_all[:, 0] < nf]
     n1 = min(len(blocks), 48)
     t = time.perf_counter()
@@ -265,7 +265,8 @@ def run_reference(a, cfg, rank):
     # box's first seconds of CPU time were measured 40 % slower)
     t = time.perf_counter()
     k = 0
-    while k < a.warmup or time.perf_counter() - t < 3.0:
+    settle = float(os.environ.get("FSE_REF_SETTLE_S", "3.0"))
+    while k < a.warmup or time.perf_counter() - t < settle:
         orc.conceal_blocks(frames, blocks, *args, nthreads=cores)
         k += 1
     t = time.perf_counter()
