@@ -578,3 +578,18 @@ def test_frames_read_from_pinned_host_memory(fse):
     assert torch.equal(plan.run(f32.cpu().pin_memory(), tile_dtype="f32").cpu(), plan.run(f32, tile_dtype="f32").cpu())
     with pytest.raises(ValueError):  # pageable host frames are refused
         plan.run(dev.cpu())
+
+
+@pytest.mark.parametrize("F,B,border,frac", [(32, 8, 8, 0.05), (128, 32, 16, 0.04)])
+def test_other_window_sizes_on_a_4k_frame(fse, F, B, border, frac):
+    """The large-batch geometries of scripts/geom_rates.py on one bench 4K u8
+    frame, every block against the C oracle: F = 32 (8 x 8 losses, 6,480
+    blocks) and F = 128 (32 x 32 losses, 322 blocks), fp32 gate."""
+    from paper_2204_14193_b200.synth import field_torch
+    frames = field_torch(1, 2160, 3840, seed=5 * 7919, device="cuda").cpu().numpy()
+    blocks = fse.frames_pattern(1, 2160, 3840, B, frac, seed=2)
+    tiles, get, plan = _run_plan(fse, frames, blocks, F, B, border, 100)
+    assert plan.info["fast_path"] == 1
+    st = fp32_gate(frames, blocks, tiles, get, F, B, border, 0.8, 0.5, 100,
+                   truth=_truth(frames, blocks, B), log=f"4k_frame_F{F}")
+    print(F, {k: v for k, v in st.items() if k != "outliers"})
