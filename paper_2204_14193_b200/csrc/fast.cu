@@ -1356,321 +1356,6 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 }
 
 
-// ------------------------------------------- F = 128, warp-specialised CTA
-// One F = 128 block's spectrum fills half the register file, so only one
-// block runs per SM and nothing overlaps its serial setup (window loads +
-// 2-D FFT, 12 % of the block time) or fills the issue slots its 8-warp
-// argmax chain leaves idle each iteration.  This CTA adds a producer warp
-// group: 4 producer warps load the NEXT block's support window and run its
-// 2-D FFT into the shared scratch while the 8 consumer warps iterate the
-// current block from registers.  Handshake by named barriers (consumers
-// arrive "scratch free" after reading a spectrum out, producers arrive
-// "spectrum ready" after writing one); the iteration trace lives in its own
-// shared buffer.  Same arithmetic as fast_kernel<128> (the spectrum, the
-// loop and the first-max are identical; the synthesis runs as one
-// coefficient group, SG = 1, whose summation order differs in the last
-// bits of the f32 tiles).
-constexpr int kWsCons = 256, kWsProd = 128, kWsTraceCap = 200;
-FSE_DEV void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-FSE_DEV void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-static size_t ws128_smem() {
-  return FG<128>::TABLE_BYTES + FG<128>::SCRATCH + 2 * (size_t)kWsTraceCap * sizeof(float4) +
-         2 * 128 * sizeof(float2) + 2 * FG<128>::NW * sizeof(uint4) + 64;
-}
-
-__global__ void __launch_bounds__(kWsCons + kWsProd, 1) fast128_ws_kernel(FastArgs a) {
-  typedef FG<128> G;
-  constexpr int F = 128, H = F / 2, ZS = F + 1, XS = H + 1;
-  extern __shared__ __align__(16) char smem[];
-  char *region = smem;                                           // W' table (planar)
-  float2 *S = (float2 *)(smem + G::TABLE_BYTES);                 // the producers' spectrum
-  float4 *trace = (float4 *)((char *)S + G::SCRATCH);            // trace | synthesis coefficients
-  float2 *syn_tw = (float2 *)(trace + 2 * kWsTraceCap);          // exp(+2 pi i j / F)
-  float2 *fft_tw = syn_tw + F;                                   // exp(-2 pi i j / F)
-  uint4 *xch = (uint4 *)(fft_tw + F);                            // 2 x NW warp candidates
-  float *e0s = (float *)(xch + 2 * G::NW);                       // e0 of the spectrum in S
-  float *pred = e0s + 4;                                         // producer e0 partials
-  const int tid = threadIdx.x;
-  for (int j = tid; j < F; j += blockDim.x) {
-    double s, c;
-    sincospi(2.0 * j / F, &s, &c);
-    syn_tw[j] = make_float2((float)c, (float)s);
-    fft_tw[j] = make_float2((float)c, (float)-s);
-  }
-  __syncthreads();
-  const int off = (F - a.B) / 2;
-
-  if (tid >= kWsCons) {
-    // ------------------------------------------------------ producer warps
-    constexpr int Q = G::QT, VPT = G::VPT, NG = kWsProd / Q, NFT = H / NG, CP = H / NG;
-    const int pt = tid - kWsCons, g = pt / Q, t = pt - (pt / Q) * Q;
-    int k = 0;
-    for (int round = blockIdx.x; round < a.n_rounds; round += gridDim.x, ++k) {
-      if (k > 0) bar_sync_n(4, kWsCons + kWsProd);  // the consumers have read the last spectrum
-      const int b = __ldg(a.rounds + round), cls = __ldg(a.round_class + round);
-      float e0p = 0.f;
-#ifndef FSE_WSDIAG
-#define FSE_WSDIAG 0
-#endif
-      if (b >= 0 && !(FSE_WSDIAG & 1)) {  // WSDIAG 1: producers skip the setup (timing only)
-        const int fidx = __ldg(a.blocks + 3 * b), top = __ldg(a.blocks + 3 * b + 1),
-                  left = __ldg(a.blocks + 3 * b + 2);
-        const int wt = top - off, wl = left - off;
-        const float *wtab = a.wtab + (size_t)cls * F * F;
-        const size_t fbase = (size_t)fidx * (size_t)a.frame_stride;
-        const int4 rect = __ldg((const int4 *)a.support_rect + cls);
-        const int j0 = rect.x >> 1, j1 = (rect.z + 1) >> 1;
-        // rows: row pairs j = g + NG fi packed as one complex row, one FFT each
-        {
-          float2 v[NFT][VPT];
-          float2 *rows[NFT];
-#pragma unroll
-          for (int fi = 0; fi < NFT; ++fi) {
-            const int j = g + NG * fi;
-            rows[fi] = S + j * ZS;
-            const bool act = j >= j0 && j < j1;
-            const int y0 = wt + 2 * j;
-#pragma unroll
-            for (int kk = 0; kk < VPT; ++kk) {
-              const int n = t + Q * kk, x = wl + n;
-              float xe = 0.f, xo = 0.f;
-              if (act && x >= 0 && x < a.W) {
-                const float we = __ldg(wtab + (2 * j) * F + n), wo = __ldg(wtab + (2 * j + 1) * F + n);
-                const bool ie = y0 >= 0 && y0 < a.H, io = y0 + 1 >= 0 && y0 + 1 < a.H;
-                const float se = ie ? load_px(a.frames, a.dtype, fbase + (size_t)y0 * a.pitch + x) : 0.f;
-                const float so = io ? load_px(a.frames, a.dtype, fbase + (size_t)(y0 + 1) * a.pitch + x) : 0.f;
-                if (we != 0.f) { xe = se * we; e0p += xe * se; }
-                if (wo != 0.f) { xo = so * wo; e0p += xo * so; }
-              }
-              v[fi][kk] = make_float2(xe, xo);
-            }
-          }
-          group_fft<F, NFT>(v, rows, 1, fft_tw, t);
-#pragma unroll
-          for (int fi = 0; fi < NFT; ++fi)
-#pragma unroll
-            for (int i = 0; i < VPT; ++i) rows[fi][group_out<F>(t, i)] = v[fi][i];
-        }
-        bar_sync_n(2, kWsProd);
-        // columns 1..H-1 of the untangled row spectra; 0 and H packed as one
-        {
-          float2 cin[CP][VPT];
-#pragma unroll
-          for (int pass = 0; pass < CP; ++pass) {
-            const int c = g + pass * NG;
-#pragma unroll
-            for (int kk = 0; kk < VPT; ++kk) {
-              const int m = t + Q * kk, j = m >> 1, odd = m & 1;
-              float2 y = make_float2(0.f, 0.f);
-              if (j >= j0 && j < j1) {
-                if (c == 0) {
-                  const float2 z0 = S[j * ZS], zh = S[j * ZS + H];
-                  y = odd ? make_float2(z0.y, zh.y) : make_float2(z0.x, zh.x);
-                } else {
-                  const float2 zl = S[j * ZS + c], zm = S[j * ZS + F - c];
-                  y = odd ? make_float2((zl.y + zm.y) * 0.5f, (zm.x - zl.x) * 0.5f)
-                          : make_float2((zl.x + zm.x) * 0.5f, (zl.y - zm.y) * 0.5f);
-                }
-              }
-              cin[pass][kk] = y;
-            }
-          }
-          bar_sync_n(2, kWsProd);  // row spectra consumed: reuse S as X
-          float2 *cols[CP];
-#pragma unroll
-          for (int pass = 0; pass < CP; ++pass) cols[pass] = S + g + pass * NG;
-          group_fft<F, CP>(cin, cols, XS, fft_tw, t);
-#pragma unroll
-          for (int pass = 0; pass < CP; ++pass) {
-            const int c = g + pass * NG;
-#pragma unroll
-            for (int i = 0; i < VPT; ++i) S[group_out<F>(t, i) * XS + c] = cin[pass][i];
-          }
-        }
-        bar_sync_n(2, kWsProd);
-        if (pt <= H) {  // untangle the packed columns 0 and H: thread r owns rows r and -r
-          const int r = pt, rm = (F - r) & (F - 1);
-          const float2 yk = S[r * XS], ym = S[rm * XS];
-          const float2 x0 = make_float2((yk.x + ym.x) * 0.5f, (yk.y - ym.y) * 0.5f);
-          const float2 xh = make_float2((yk.y + ym.y) * 0.5f, (ym.x - yk.x) * 0.5f);
-          S[r * XS] = x0;
-          S[r * XS + H] = xh;
-          if (rm != r) {
-            S[rm * XS] = make_float2(x0.x, -x0.y);
-            S[rm * XS + H] = make_float2(xh.x, -xh.y);
-          }
-        }
-      }
-      for (int o = 16; o; o >>= 1) e0p += __shfl_xor_sync(0xffffffffu, e0p, o);
-      if ((pt & 31) == 0) pred[pt >> 5] = e0p;
-      bar_sync_n(2, kWsProd);
-      if (pt == 0) e0s[0] = pred[0] + pred[1] + pred[2] + pred[3];
-      bar_arrive_n(3, kWsCons + kWsProd);  // the spectrum of this round is in S
-    }
-    return;
-  }
-
-  // ------------------------------------------------------- consumer warps
-  const int st = tid, w = st >> 5, lane = st & 31;
-  int loaded = -1;
-  float4 *const cq = trace + kWsTraceCap;
-  for (int round = blockIdx.x; round < a.n_rounds; round += gridDim.x) {
-    const int cls = __ldg(a.round_class + round);
-    const int b = __ldg(a.rounds + round);
-    if (cls != loaded) {
-      bar_sync_n(1, kWsCons);
-      copy_table(region, (const char *)a.table + (size_t)cls * a.table_bytes, a.table_bytes, st, kWsCons);
-      bar_sync_n(1, kWsCons);
-      loaded = cls;
-    }
-    bar_sync_n(3, kWsCons + kWsProd);  // this round's spectrum is ready
-    float2 Rre[G::NP], Rim[G::NP];
-    const float e0 = e0s[0];
-    {
-      auto bin = [&](int r, int c) -> float2 {
-        const bool lo = c <= H;
-        const float2 z = S[lo ? r * XS + c : ((F - r) & (F - 1)) * XS + (F - c)];
-        return make_float2(z.x, lo ? z.y : -z.y);
-      };
-#pragma unroll
-      for (int p = 0; p < G::NP; ++p) {
-        const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
-        const float2 xa = bin(ia >> G::LOG, ia & (F - 1)), xb = bin(ib >> G::LOG, ib & (F - 1));
-        Rre[p] = __fadd2_rn(make_float2(xa.x, xb.x), make_float2(0.f, 0.f));
-        Rim[p] = __fadd2_rn(make_float2(xa.y, xb.y), make_float2(0.f, 0.f));
-      }
-    }
-    if (round + gridDim.x < a.n_rounds) bar_arrive_n(4, kWsCons + kWsProd);  // S free for the next block
-    if (b < 0) continue;
-
-    // ------------------------------------------------------- iterations
-    const float ginv = a.gamma * __ldg(a.inv_w00 + cls);
-    float cre = 0.f, cim = 0.f;
-    unsigned gidx = 0;
-    unsigned xc = (unsigned)__cvta_generic_to_shared(xch);
-    const int rowbase = w * G::RPW;
-    const float *Tre = (const float *)region;
-    const float *Tim = Tre + G::TROWS * F;
-#pragma unroll 1
-    for (int it = 0; it < a.iterations; ++it) {
-      const int rowoff = (rowbase - (int)(gidx >> G::LOG)) & (F - 1);
-      float bst = -1.f, bxs = 0.f;
-      int bps = 0;
-      int co[4];
-#pragma unroll
-      for (int h = 0; h < 4; ++h) co[h] = (lane + 32 * h - (int)(gidx & (F - 1))) & (F - 1);
-#pragma unroll
-      for (int p = 0; p < G::NP; ++p) {
-        const int r = (rowoff + (p >> 1)) * F;
-        const int q = 2 * (p & 1);
-        const float2 wr = make_float2(Tre[r + co[q]], Tre[r + co[q + 1]]);
-        const float2 wi = make_float2(Tim[r + co[q]], Tim[r + co[q + 1]]);
-        ffma2_acc(Rre[p], wr, -cre);
-        ffma2_acc(Rre[p], wi, cim);
-        ffma2_acc(Rim[p], wi, -cre);
-        ffma2_acc(Rim[p], wr, -cim);
-        float2 mg = fmul2(Rre[p], Rre[p]);
-        mg = ffma2(Rim[p], Rim[p], mg);
-        first_max(bst, bps, bxs, mg, p);
-      }
-      const int myidx = bin_index<F>(w, lane, bps, bxs >= bst ? 0 : 1);
-      const unsigned key = __float_as_uint(bst);
-      const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
-      const unsigned widx = __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
-      int pw, mw, ow;
-      decode_bin<F>((int)widx, w, pw, mw, ow);
-      float are, aim;
-      pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
-      are = __shfl_sync(0xffffffffu, are, ow);
-      aim = __shfl_sync(0xffffffffu, aim, ow);
-      if (lane == 0) sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
-      bar_sync_n(1, kWsCons);
-      uint4 cd[G::NW];
-#pragma unroll
-      for (int j = 0; j < G::NW; ++j) cd[j] = lds128u(xc + 16u * (unsigned)j);
-#pragma unroll
-      for (int s = 1; s < G::NW; s *= 2)
-#pragma unroll
-        for (int j = 0; j + s < G::NW; j += 2 * s)
-          if (cd[j + s].x > cd[j].x) cd[j] = cd[j + s];
-      gidx = cd[0].y;
-      are = __uint_as_float(cd[0].z);
-      aim = __uint_as_float(cd[0].w);
-      xc ^= (unsigned)(G::NW * sizeof(uint4));
-      cre = ginv * are;
-      cim = ginv * aim;
-      if (st == 0) trace[it] = make_float4(__uint_as_float(gidx), are, aim, 0.f);
-    }
-    bar_sync_n(1, kWsCons);
-
-    // ------------------------------------ coefficients, trace, synthesis
-    for (int k2 = st; k2 < a.iterations; k2 += kWsCons) {
-      const float4 tr = trace[k2];
-      const unsigned gi = __float_as_uint(tr.x), tu = gi >> G::LOG;
-      const float cr = ginv * tr.y, ci = ginv * tr.z;
-      trace[k2] = make_float4(__uint_as_float(tu | ((gi & (F - 1)) << 16)), cr, ci, tr.y * tr.y + tr.z * tr.z);
-      const float2 om = syn_tw[(tu * (G::B / 2)) & (F - 1)];
-      cq[k2] = make_float4(cr, cr * om.x - ci * om.y, -ci, -(cr * om.y + ci * om.x));
-    }
-    bar_sync_n(1, kWsCons);
-    if (a.trace_uv && st == 0) {
-      const float dinv = a.gamma * (2.f - a.gamma) * __ldg(a.inv_w00 + cls);
-      float e = e0;
-      for (int it = 0; it < a.iterations; ++it) {
-        const size_t o = (size_t)b * a.iterations + it;
-        const float4 tr = trace[it];
-        const unsigned uv = __float_as_uint(tr.x);
-        e -= dinv * tr.w;
-        a.trace_uv[2 * o] = (int)(uv & 0xffffu);
-        a.trace_uv[2 * o + 1] = (int)(uv >> 16);
-        a.trace_e[o] = e;
-        a.trace_c[2 * o] = tr.y;
-        a.trace_c[2 * o + 1] = tr.z;
-      }
-    }
-    // synthesis, one coefficient group (SG = 1): thread gt owns pixel pairs
-    // (m, n), (m + B/2, n), m = m0 + RS kk; twiddles by recurrence
-    constexpr int BB = G::B * G::B, GT = kWsCons, PP = BB / GT / 2, RS = GT / G::B;
-    static_assert(PP * GT * 2 == BB, "pixel pairs cover the block");
-    const int pm = off + st / G::B, pn = off + st % G::B;
-    float2 gacc[PP];
-#pragma unroll
-    for (int kk = 0; kk < PP; ++kk) gacc[kk] = make_float2(0.f, 0.f);
-#pragma unroll 2
-    for (int it = 0; it < a.iterations; ++it) {
-      const unsigned uv = __float_as_uint(((const float *)trace)[4 * it]);
-      const float4 c4 = cq[it];
-      const float2 cr = make_float2(c4.x, c4.y), ci = make_float2(c4.z, c4.w);
-      const int tu = (int)(uv & 0xffffu), j0 = tu * pm + (int)(uv >> 16) * pn;
-      float2 tt = syn_tw[j0 & (F - 1)];
-      const float2 wv = syn_tw[(tu * RS) & (F - 1)];
-      const float2 wa = make_float2(wv.x, wv.y), wb = make_float2(-wv.y, wv.x);
-#pragma unroll
-      for (int kk = 0; kk < PP; ++kk) {
-        gacc[kk] = ffma2(cr, make_float2(tt.x, tt.x), gacc[kk]);
-        gacc[kk] = ffma2(ci, make_float2(tt.y, tt.y), gacc[kk]);
-        if (kk + 1 < PP) tt = ffma2(make_float2(tt.y, tt.y), wb, fmul2(make_float2(tt.x, tt.x), wa));
-      }
-    }
-    auto store_px = [&](int qq, float gk) {
-      const size_t o = (size_t)b * BB + (size_t)qq;
-      if (a.tile_dtype == 0) {
-        ((uint8_t *)a.tiles)[o] = (uint8_t)__float2int_rn(fminf(fmaxf(gk, 0.f), 255.f));
-      } else if (a.tile_dtype == 1) {
-        ((float *)a.tiles)[o] = gk;
-      } else {
-        ((double *)a.tiles)[o] = (double)gk;
-      }
-    };
-#pragma unroll
-    for (int kk = 0; kk < PP; ++kk) {
-      store_px(st + GT * kk, gacc[kk].x);
-      store_px(st + GT * kk + BB / 2, gacc[kk].y);
-    }
-    bar_sync_n(1, kWsCons);  // trace reuse by the next block
-  }
-}
 
 template <int F, int ALG = 0> static size_t fast_smem(int iter_cap) {
   (void)iter_cap;
@@ -1704,18 +1389,6 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algor
       smem = fast_smem<64>(0); tb = FG<64>::TABLE_BYTES; S = FG<64>::S;
       break;
     case 128: {
-      // the warp-specialised CTA (fast128_ws_kernel) when its shared trace
-      // holds the iterations; FSE_WS128=0 selects the plain kernel
-      const char *ws = getenv("FSE_WS128");
-      if (iterations <= kWsTraceCap && !(ws && atoi(ws) == 0) && ws128_smem() <= 227 * 1024) {
-        cfg->global_trace = false;
-        cfg->slots = 1;
-        cfg->threads = kWsCons + kWsProd;
-        cfg->smem_bytes = (int)ws128_smem();
-        cfg->grid = sm_count;
-        cfg->table_bytes = FG<128>::TABLE_BYTES;
-        return true;
-      }
       cfg->global_trace = iterations > FG<128>::TRACE_CAP;
       smem = fast_smem<128>(0); tb = FG<128>::TABLE_BYTES; S = FG<128>::S;
       break;
@@ -1752,15 +1425,6 @@ cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensor
     return a.F == 64   ? launch_fast_t<64, 1>(a, cfg, tmap, s)
            : a.F == 32 ? launch_fast_t<32, 1>(a, cfg, tmap, s)
                        : cudaErrorInvalidValue;
-  if (a.F == 128 && cfg.threads == kWsCons + kWsProd) {
-    cudaError_t e = cudaFuncSetAttribute(fast128_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         cfg.smem_bytes);
-    if (e != cudaSuccess) return e;
-    const int grid = cfg.grid < a.n_rounds ? cfg.grid : a.n_rounds;
-    if (grid <= 0) return cudaSuccess;
-    fast128_ws_kernel<<<grid, cfg.threads, cfg.smem_bytes, s>>>(a);
-    return cudaGetLastError();
-  }
   switch (a.F) {
     case 32: return launch_fast_t<32, 0>(a, cfg, tmap, s);
     case 64: return launch_fast_t<64, 0>(a, cfg, tmap, s);
