@@ -49,6 +49,32 @@ __device__ double block_max(double v, double *red) {
   return v;
 }
 
+// block-wide maximum of mx and sum of sm in one reduction (every thread gets
+// both; the sum's association order is that of block_sum)
+__device__ void block_max_sum(double &mx, double &sm, double *red) {
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = mx; red[32 + (threadIdx.x >> 5)] = sm; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const bool v = threadIdx.x < (blockDim.x >> 5);
+    mx = v ? red[threadIdx.x] : 0.0;
+    sm = v ? red[32 + threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    }
+    if (threadIdx.x == 0) { red[0] = mx; red[32] = sm; }
+  }
+  __syncthreads();
+  mx = red[0];
+  sm = red[32];
+  __syncthreads();
+}
+
 // max |x[i]| over the samples with lab[i] == keep (all when lab is null)
 __device__ double block_max_abs(const double *x, int n, double *red, const int8_t *lab = nullptr,
                                 int keep = 0) {
@@ -240,6 +266,27 @@ template <typename T> FSE_DEV unsigned warp_first_max(T v, unsigned idx, bool va
   return __reduce_min_sync(0xffffffffu, valid && h == wh && l == wl ? idx : 0xffffffffu);
 }
 
+// warp_first_max with the winner's lane: one REDUX on the high key word and
+// a ballot settle the common case (a single lane holds the largest high
+// word); only exact high-word ties take the full (lo word, index) path.
+// The same total order as warp_first_max.
+template <typename T>
+FSE_DEV unsigned warp_first_max_lane(T v, unsigned idx, bool valid, int &lane_out) {
+  const unsigned h = valid ? Key<T>::hi(v) : 0u;
+  const unsigned wh = __reduce_max_sync(0xffffffffu, h);
+  const unsigned tie = __ballot_sync(0xffffffffu, valid && h == wh);
+  if (__popc(tie) == 1) {
+    lane_out = __ffs(tie) - 1;
+    return __shfl_sync(0xffffffffu, idx, lane_out);
+  }
+  const unsigned l = valid ? Key<T>::lo(v) : 0u;
+  unsigned wl = 0u;
+  if (sizeof(T) == 8) wl = __reduce_max_sync(0xffffffffu, h == wh ? l : 0u);
+  const unsigned widx = __reduce_min_sync(0xffffffffu, valid && h == wh && l == wl ? idx : 0xffffffffu);
+  lane_out = __ffs(__ballot_sync(0xffffffffu, valid && idx == widx)) - 1;
+  return widx;
+}
+
 // one vector load of a complex value (16 B for double: LDS.128, not two LDS.64)
 FSE_DEV Cplx<double> load_cplx(const Cplx<double> *p) {
   const double2 v = *(const double2 *)p;
@@ -383,17 +430,18 @@ __device__ void cfse_iterate_tile(const Cplx<T> *R0, const Cplx<T> *W, Cplx<T> *
 #endif
   for (int it = 0; it < iterations; ++it) {
     double4 *slot = cand + (it & 1) * NW;
-    const unsigned widx = warp_first_max<T>(best, (unsigned)bi, true);
+    int wl_own;
+    warp_first_max_lane<T>(best, (unsigned)bi, true, wl_own);
     FSE_LCLK(0);
-    if ((unsigned)bi == widx)
+    if (lane == wl_own)
       slot[w] = make_double4((double)best, __longlong_as_double((long long)bi), (double)bre, (double)bim);
     FSE_LCLK(1);
     __syncthreads();
     FSE_LCLK(2);
     const double4 c4 = lane < NW ? slot[lane] : make_double4(-1.0, __longlong_as_double(-1ll), 0.0, 0.0);
     const unsigned cidx = (unsigned)__double_as_longlong(c4.y);
-    const unsigned gidx = warp_first_max<T>((T)c4.x, cidx, c4.x >= 0.0);
-    const int ow = __ffs(__ballot_sync(0xffffffffu, lane < NW && cidx == gidx)) - 1;
+    int ow;
+    const unsigned gidx = warp_first_max_lane<T>((T)c4.x, cidx, c4.x >= 0.0, ow);
     const T ar = (T)__shfl_sync(0xffffffffu, c4.z, ow);
     const T ai = (T)__shfl_sync(0xffffffffu, c4.w, ow);
     const int u = (int)gidx >> logN, v = (int)gidx & (N - 1);
@@ -704,26 +752,28 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
   // w = 0, so this equals the reference for finite input, and a non-finite
   // value in the lost block (common for decoded frames) cannot leak into
   // the window through 0 * NaN.
-  double smax = 0.0;
-  for (int i = threadIdx.x; i < MN; i += blockDim.x)
-    if (lab[i] == kSupport) smax = fmax(smax, fabs(sval(i)));
-  smax = block_max(smax, red);
-  FSE_GSTOP(1);
-  int ex = 0;
-  if (smax > 0.0) frexp(smax, &ex);
-  const double kappa = ldexp(1.0, -ex), inv_kappa = ldexp(1.0, ex);
-  double e0p = 0.0;
+  // one pass over the window: w, s*w (unscaled) into A, max |s| over the
+  // support and e0 = sum w s^2 (cfse.py:51); then one joint reduction and
+  // the exact power-of-two scaling of the packed signal
+  double smax = 0.0, e0p = 0.0;
   for (int i = threadIdx.x; i < MN; i += blockDim.x) {
     int m = i / N, n = i - m * N;
     const bool sup = lab[i] == kSupport;
     double w = !sup ? 0.0 : a.wtab ? a.wtab[(size_t)a.label_index[win] * a.labels_stride + i]
                                    : weight_at(m, n, M, N, a.rho);
     const double si = sup ? sval(i) : 0.0;
-    double sw = si * w;
-    A[i] = make_double2(w, sw * kappa);
-    e0p += w * si * si;  // np.sum(w * s * s), cfse.py:51
+    smax = fmax(smax, fabs(si));
+    A[i] = make_double2(w, si * w);
+    e0p += w * si * si;
   }
-  const double e0 = block_sum(e0p, red);  // includes barrier
+  double e0 = e0p;
+  block_max_sum(smax, e0, red);  // includes barriers
+  FSE_GSTOP(1);
+  int ex = 0;
+  if (smax > 0.0) frexp(smax, &ex);
+  const double kappa = ldexp(1.0, -ex), inv_kappa = ldexp(1.0, ex);
+  for (int i = threadIdx.x; i < MN; i += blockDim.x) A[i].y *= kappa;  // exact
+  __syncthreads();
   FSE_GSTOP(2);
   // power-of-two sizes: in-place radix-2 FFTs (log-depth, a few us for 64 x
   // 64); other sizes: the separable direct DFT
@@ -808,21 +858,73 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
   // 145), then inverse FFTs and 1/(MN) -- or, for other sizes, the direct
   // sum g = sum c e^{+2 pi i (u m/M + v n/N)} over the trace
   double *model = a.model ? a.model + (size_t)win * 2 * MN : nullptr;
+  FSE_GSTOP(5);
+  if (pow2 && img && !model && M == N && (kGenThreads % (a.B * a.B)) == 0) {
+    // image mode needs Re{g} on the B x B loss tile only: a direct sum over
+    // the trace there is ~10x cheaper than the inverse 2-D FFT of G.  TPP
+    // threads per pixel split the iterations (strided) and meet by shuffles;
+    // e^{2 pi i (u m + v n) / M} is one table lookup (M == N)
+    __syncthreads();  // trace (global, written by thread 0) visible
+    // stage (u, v, c, pair factor) in shared memory with one coalesced pass:
+    // the sum below then reads broadcasts, not serial L2 round trips
+    const bool staged = (size_t)n_it * sizeof(double4) <= (size_t)MN * sizeof(double2);
+    double4 *tr4 = (double4 *)Bf;
+    if (staged) {
+      for (int it = threadIdx.x; it < n_it; it += blockDim.x) {
+        const double f = (ALG == 1 && !a.selfs[(size_t)win * a.iterations + it]) ? 2.0 : 1.0;
+        tr4[it] = make_double4(cs[2 * it] * f, cs[2 * it + 1] * f, (double)us[it], (double)vs[it]);
+      }
+      __syncthreads();
+    }
+    const int BB = a.B * a.B, TPP = kGenThreads / BB;  // power of two (B is), <= 32 for B >= 4
+    const int px = threadIdx.x / TPP, sub = threadIdx.x - px * TPP;
+    const int m = off + px / a.B, n = off + px % a.B;
+    double g = 0.0;
+#pragma unroll 4
+    for (int it = sub; it < n_it; it += TPP) {
+      double4 t4;
+      if (staged) {
+        t4 = tr4[it];
+      } else {
+        const double f = (ALG == 1 && !a.selfs[(size_t)win * a.iterations + it]) ? 2.0 : 1.0;
+        t4 = make_double4(cs[2 * it] * f, cs[2 * it + 1] * f, (double)us[it], (double)vs[it]);
+      }
+      const double2 ph = twMp[((int)t4.z * m + (int)t4.w * n) & (M - 1)];
+      g += t4.x * ph.x - t4.y * ph.y;  // Re{c phi} (x2 for a conjugate pair)
+    }
+    for (int o = TPP >> 1; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+    if (sub == 0) put(m * N + n, g, true);
+    FSE_GSTOP(6);
+    FSE_GSTOP(7);
+    return;
+  }
   if (pow2) {
-    FSE_GSTOP(5);
-    __syncthreads();  // trace (global, written by thread 0) visible; A free
+    __syncthreads();  // trace (global, written by thread 0) visible; A and Bf free
+    // stage the trace in shared memory (Bf) with one coalesced pass, so the
+    // in-order scatter below reads broadcasts instead of L2 round trips
+    const bool staged = (size_t)n_it * 24 <= (size_t)MN * sizeof(double2);
+    double2 *tc = (double2 *)Bf;
+    int *ti = (int *)(tc + n_it), *tsf = ti + n_it;
+    if (staged)
+      for (int it = threadIdx.x; it < n_it; it += blockDim.x) {
+        tc[it] = make_double2(cs[2 * it], cs[2 * it + 1]);
+        ti[it] = (int)us[it] * N + (int)vs[it];
+        tsf[it] = ALG == 1 ? a.selfs[(size_t)win * a.iterations + it] : 1;
+      }
     for (int i = threadIdx.x; i < MN; i += blockDim.x) A[i] = make_double2(0.0, 0.0);
     __syncthreads();
     const double dmn = (double)MN;
     for (int it = 0; it < n_it; ++it) {  // each bin accumulated by one thread, in order
-      const int idx = (int)us[it] * N + (int)vs[it];
-      const double cr = cs[2 * it], ci = cs[2 * it + 1];
+      const int idx = staged ? ti[it] : (int)us[it] * N + (int)vs[it];
+      const double2 c = staged ? tc[it] : make_double2(cs[2 * it], cs[2 * it + 1]);
+      const double cr = c.x, ci = c.y;
       if ((idx & (kGenThreads - 1)) == (int)threadIdx.x) {
         A[idx].x = __dadd_rn(A[idx].x, __dmul_rn(dmn, cr));
         A[idx].y = __dadd_rn(A[idx].y, __dmul_rn(dmn, ci));
       }
-      if (ALG == 1 && !a.selfs[(size_t)win * a.iterations + it]) {
-        const int mi = ((M - (int)us[it]) & (M - 1)) * N + ((N - (int)vs[it]) & (N - 1));
+      if (ALG == 1 && !(staged ? tsf[it] : a.selfs[(size_t)win * a.iterations + it])) {
+        const int u = idx / N, v = idx - u * N;
+        const int mi = ((M - u) & (M - 1)) * N + ((N - v) & (N - 1));
         if ((mi & (kGenThreads - 1)) == (int)threadIdx.x) {
           A[mi].x = __dadd_rn(A[mi].x, __dmul_rn(dmn, cr));
           A[mi].y = __dadd_rn(A[mi].y, __dmul_rn(dmn, -ci));
