@@ -5,6 +5,15 @@
 
 #define FSE_DEV __device__ __forceinline__
 
+// FSE_CHECKS builds (tests only): device-side bounds checks on the shared and
+// global indices of the kernels (compute-sanitizer is closed on this pool).
+#ifdef FSE_CHECKS
+#include <cassert>
+#define FSE_CHECK(cond) assert(cond)
+#else
+#define FSE_CHECK(cond) ((void)0)
+#endif
+
 namespace fse {
 
 constexpr int kPadding = 0;

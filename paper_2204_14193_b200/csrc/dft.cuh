@@ -119,7 +119,10 @@ inline __device__ void fft64_axis(double2 *A, double2 *X, bool cols, bool invers
   // transform f, lane q: rows -> f = t >> 3, q = t & 7; cols -> f = t & 63, q = t >> 6
   const int f = cols ? (t & 63) : (t >> 3), q = cols ? (t >> 6) : (t & 7);
   // element n of transform f
-  auto at = [&](int n) -> double2 & { return cols ? A[n * 64 + f] : A[f * 64 + n]; };
+  auto at = [&](int n) -> double2 & {
+    FSE_CHECK(n >= 0 && n < 64 && f >= 0 && f < 64);
+    return cols ? A[n * 64 + f] : A[f * 64 + n];
+  };
   // exchange slot of (q1, k1) of transform f
   auto ex = [&](int q1, int k1) -> double2 & {
     return cols ? X[(q1 * 8 + k1) * 64 + f] : X[f * 64 + q1 * 8 + (k1 ^ q1)];

@@ -92,15 +92,6 @@ template <int F> struct FG {
   static constexpr size_t REGION = TABLE_BYTES;
 };
 
-// FSE_CHECKS builds (tests only): device-side bounds checks on every shared
-// and global index of the fused kernel (compute-sanitizer is not available
-// on this pool).
-#ifdef FSE_CHECKS
-#include <cassert>
-#define FSE_CHECK(cond) assert(cond)
-#else
-#define FSE_CHECK(cond) ((void)0)
-#endif
 
 FSE_DEV float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 // acc = a * b + acc with the accumulator as a read-write PTX operand.  With

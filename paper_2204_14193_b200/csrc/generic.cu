@@ -467,6 +467,7 @@ __device__ void cfse_iterate_tile(const Cplx<T> *R0, const Cplx<T> *W, Cplx<T> *
     bi = 0;
 #pragma unroll
     for (int j = 0; j < BPT; ++j) {
+      FSE_CHECK((wp - wx) + kGenThreads * j < 2 * MN);
       const Cplx<T> wv = load_cplx(wp + kGenThreads * j);
       Cplx<T> x = R[j];
       T pr = F::sub(F::mul(cr, wv.re), F::mul(ci, wv.im));
@@ -722,6 +723,7 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     }
     if (!loss) return;
     const int m = i / N, n = i - m * N;
+    FSE_CHECK(m >= off && m < off + a.B && n >= off && n < off + a.B);
     const size_t o = (size_t)win * a.B * a.B + (size_t)(m - off) * a.B + (n - off);
     if (a.tile_dtype == 0)
       ((uint8_t *)a.tiles)[o] = (uint8_t)__double2int_rn(fmin(fmax(v, 0.0), 255.0));
@@ -872,6 +874,7 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
     if (staged) {
       for (int it = threadIdx.x; it < n_it; it += blockDim.x) {
         const double f = (ALG == 1 && !a.selfs[(size_t)win * a.iterations + it]) ? 2.0 : 1.0;
+        FSE_CHECK((it + 1) * sizeof(double4) <= (size_t)MN * sizeof(double2));
         tr4[it] = make_double4(cs[2 * it] * f, cs[2 * it + 1] * f, (double)us[it], (double)vs[it]);
       }
       __syncthreads();
@@ -918,6 +921,7 @@ __global__ void __launch_bounds__(kGenThreads) extrapolate_kernel(GenArgs a, Gen
       const int idx = staged ? ti[it] : (int)us[it] * N + (int)vs[it];
       const double2 c = staged ? tc[it] : make_double2(cs[2 * it], cs[2 * it + 1]);
       const double cr = c.x, ci = c.y;
+      FSE_CHECK(idx >= 0 && idx < MN);
       if ((idx & (kGenThreads - 1)) == (int)threadIdx.x) {
         A[idx].x = __dadd_rn(A[idx].x, __dmul_rn(dmn, cr));
         A[idx].y = __dadd_rn(A[idx].y, __dmul_rn(dmn, ci));
