@@ -236,6 +236,43 @@ class Concealer:
         needs blocks in frame order.  Returns out.numpy()."""
         import torch
 
+        dst = self._dst(out)
+        self._enqueue(host_frames, dst)
+        for ks in self.compute_streams:
+            ks.synchronize()
+        return self._result(dst, copy)
+
+    def capture(self, host_frames, out=None):
+        """Record the whole pipeline for these buffers (pinned host frames, and
+        `out` or the internal tile buffer) as one CUDA graph and return a
+        callable that replays it: each call conceals the current contents of
+        `host_frames` with a single graph launch instead of one host round of
+        copies and launches per chunk, and returns the tiles as `run` does.
+        For decoders that refill the same pinned frame buffer every batch."""
+        import torch
+
+        dst = self._dst(out)
+        self.run(host_frames, out=out)  # warm-up: function attributes, tensor maps
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        side = (self.copy_stream, *self.compute_streams)
+        with torch.cuda.graph(graph, stream=cap):
+            for s in side:  # fork the side streams from the capture stream ...
+                s.wait_stream(cap)
+            self._enqueue(host_frames, dst)
+            for s in side:  # ... and join them back
+                cap.wait_stream(s)
+        self._graphs = getattr(self, "_graphs", []) + [graph]  # keep it alive with the Concealer
+
+        def replay(copy: bool = False) -> np.ndarray:
+            graph.replay()
+            torch.cuda.current_stream().synchronize()
+            return self._result(dst, copy)
+
+        return replay
+
+    def _dst(self, out):
         dst = self.host_tiles
         if out is not None:
             if not self.identity_order:
@@ -243,6 +280,20 @@ class Concealer:
             if tuple(out.shape) != tuple(dst.shape) or out.dtype != dst.dtype or not out.is_pinned():
                 raise ValueError(f"out must be a pinned {dst.dtype} tensor of shape {tuple(dst.shape)}")
             dst = out
+        return dst
+
+    def _result(self, dst, copy: bool) -> np.ndarray:
+        tiles = dst.numpy()
+        if self.identity_order:
+            return tiles.copy() if copy else tiles
+        res = np.empty(tiles.shape, tiles.dtype)
+        res[self.order] = tiles
+        return res
+
+    def _enqueue(self, host_frames, dst) -> None:
+        """Queue every chunk's H2D copy and kernel on the copy / compute streams."""
+        import torch
+
         cs = self.copy_stream
         nb = len(self.dev_frames)
         done = [None] * len(self.chunks)  # compute-done event per chunk (frees its buffer)
@@ -267,14 +318,6 @@ class Concealer:
                 ev = torch.cuda.Event()
                 ev.record(ks)
                 done[i] = ev
-        for ks in self.compute_streams:
-            ks.synchronize()
-        tiles = dst.numpy()
-        if self.identity_order:
-            return tiles.copy() if copy else tiles
-        res = np.empty(tiles.shape, tiles.dtype)
-        res[self.order] = tiles
-        return res
 
 
 def conceal_frames(frames, blocks, geometry: Geometry = Geometry(), *, rho_hat=0.8, gamma=0.2,

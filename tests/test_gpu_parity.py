@@ -593,3 +593,22 @@ def test_other_window_sizes_on_a_4k_frame(fse, F, B, border, frac):
     st = fp32_gate(frames, blocks, tiles, get, F, B, border, 0.8, 0.5, 100,
                    truth=_truth(frames, blocks, B), log=f"4k_frame_F{F}")
     print(F, {k: v for k, v in st.items() if k != "outliers"})
+
+
+def test_concealer_graph_replay(fse):
+    """Concealer.capture records the chunked H2D + kernel pipeline as one CUDA
+    graph; replays conceal the current contents of the pinned frame buffer
+    (refilled between calls) exactly like run()."""
+    from paper_2204_14193_b200.synth import frame_u8
+    frames = np.stack([frame_u8(270, 480, seed=80 + f) for f in range(5)])
+    blocks = fse.frames_pattern(5, 270, 480, 16, 0.05, seed=11)
+    con = fse.Concealer(blocks, 5, 270, 480, chunk_frames=2, iterations=60, gamma=0.5)
+    host = con.pin(frames)
+    replay = con.capture(host)
+    a = replay(copy=True)
+    assert np.array_equal(a, con.run(host, copy=True))
+    frames2 = np.stack([frame_u8(270, 480, seed=90 + f) for f in range(5)])
+    host.copy_(__import__("torch").from_numpy(frames2))  # refill the same pinned buffer
+    b = replay(copy=True)
+    assert not np.array_equal(a, b)
+    assert np.array_equal(b, con.run(con.pin(frames2), copy=True))
