@@ -263,9 +263,8 @@ class Concealer:
             self._enqueue(host_frames, dst)
             for s in side:  # ... and join them back
                 cap.wait_stream(s)
-        self._graphs = getattr(self, "_graphs", []) + [graph]  # keep it alive with the Concealer
 
-        def replay(copy: bool = False) -> np.ndarray:
+        def replay(copy: bool = False) -> np.ndarray:  # holds the graph alive
             graph.replay()
             torch.cuda.current_stream().synchronize()
             return self._result(dst, copy)
