@@ -153,6 +153,8 @@ typedef struct {
   int grid;        /* CTAs launched (persistent)                         */
   int smem_bytes;  /* dynamic shared memory per CTA                      */
   int fast_path;   /* 1 = fused register-resident fp32 kernel            */
+  int n_centred;   /* classes iterated in the centred frame (mirror-      */
+                   /* symmetric weights: one real table value per bin)    */
 } fse_plan_info;
 
 /* blocks: HOST int32 n x 3 (frame, top, left).  F in {32, 64, 128} for the

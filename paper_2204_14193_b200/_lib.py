@@ -37,7 +37,7 @@ class FseCudaError(FseError, RuntimeError):
 
 class PlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
-        "n_blocks", "n_classes", "n_rounds", "slots", "threads", "grid", "smem_bytes", "fast_path")]
+        "n_blocks", "n_classes", "n_rounds", "slots", "threads", "grid", "smem_bytes", "fast_path", "n_centred")]
 
 
 _lib = None

@@ -107,6 +107,8 @@ struct fse_plan {
   // device
   int32_t *blocks = nullptr, *rounds = nullptr, *round_class = nullptr, *block_class = nullptr;
   int32_t *rects = nullptr;  // n_classes x (r0, c0, r1, c1): clipped support rectangle
+  int32_t *class_sym = nullptr;  // n_classes: fused-kernel table in the centred frame (real Q)
+  int n_sym = 0;                 // classes with the centred-frame table
   int8_t *labels = nullptr;
   float *wtab = nullptr, *inv_w00 = nullptr;
   void *table = nullptr;
@@ -392,7 +394,30 @@ int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int 
   if (p->fast && p->cfg.global_trace)
     CK(p->alloc(&p->trace_scratch, (size_t)p->cfg.grid * p->cfg.slots * 2 * iterations));
 
+  // Centred frame (fast.cu): a class whose label map is mirror-symmetric in
+  // both axes (every unclipped window) has real centred weight spectra; the
+  // fused cFSE kernel then iterates on one real table value per bin.
+  // FSE_SYM=0 keeps every class on the complex W' table.
+  std::vector<int32_t> sym(std::max(nc, 1), 0);
+  {
+    const char *sym_env = getenv("FSE_SYM");
+    const bool allow = p->fast && algorithm == FSE_ALG_CFSE && (F == 32 || F == 64) &&
+                       !(sym_env && atoi(sym_env) == 0);
+    for (int c = 0; allow && c < nc; ++c) {
+      const int8_t *L = labels.data() + (size_t)c * F * F;
+      bool ok = true;
+      for (int m = 0; ok && m < F; ++m)
+        for (int n = 0; ok && n < F; ++n)
+          ok = L[m * F + n] == L[(F - 1 - m) * F + n] && L[m * F + n] == L[m * F + (F - 1 - n)];
+      sym[c] = ok;
+      p->n_sym += ok;
+    }
+  }
+  CK(p->alloc(&p->class_sym, (size_t)std::max(nc, 1)));
+  CK(cudaMemcpyAsync(p->class_sym, sym.data(), (size_t)std::max(nc, 1) * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, st));
   fse::ClassSetupArgs ca{};
+  ca.sym = p->class_sym;
   ca.n_classes = nc; ca.F = F; ca.rho = rho; ca.labels = p->labels; ca.W64 = p->W64;
   ca.w64 = p->w64; ca.wtab = p->wtab; ca.fast_table = p->fast ? p->table : nullptr;
   ca.fast_table_bytes = p->fast ? p->cfg.table_bytes : 0; ca.w00 = p->w00; ca.tmp = p->tmp;
@@ -485,6 +510,7 @@ int fse_plan_get_info(const fse_plan *p, fse_plan_info *info) {
   info->grid = p->fast ? std::min(p->cfg.grid, p->n_rounds) : p->chunk;
   info->smem_bytes = p->fast ? p->cfg.smem_bytes : 0;
   info->fast_path = p->fast ? 1 : 0;
+  info->n_centred = p->n_sym;
   return FSE_OK;
 }
 
@@ -521,6 +547,7 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
     a.n_blocks = p->n_blocks; a.n_classes = p->n_classes;
     a.round_class = p->round_class; a.blocks = p->blocks; a.wtab = p->wtab; a.table = p->table;
     a.table_bytes = p->cfg.table_bytes; a.inv_w00 = p->inv_w00; a.support_rect = p->rects;
+    a.class_sym = p->class_sym;
     a.frames = frames; a.dtype = dtype; a.pitch = pitch; a.frame_stride = frame_stride;
     a.H = p->H; a.W = p->W; a.tiles = tiles; a.tile_dtype = tile_dtype;
     a.trace_uv = trace_uv; a.trace_c = (float *)trace_c; a.trace_e = (float *)trace_e;

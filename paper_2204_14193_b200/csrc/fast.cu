@@ -40,6 +40,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "dft.cuh"
 #include "kernels.h"
@@ -90,6 +92,11 @@ template <int F> struct FG {
   // transforms per lane group and pass: every row pair / column in one pass
   static constexpr int NFT = (F / 2) / (NT / QT);
   static constexpr size_t REGION = TABLE_BYTES;
+  // centred-frame real table (mirror-symmetric classes, F = 32 / 64): SYM_R x
+  // SYM_C float2 entries, rows i = r - (F - 1), columns j = c - (F - 1)
+  static constexpr int SYM_R = F == 32 ? 62 : 2 * F - 1;
+  static constexpr int SYM_C = F == 32 ? 63 : F + 31;
+  static_assert(F == 128 || (size_t)SYM_R * SYM_C * sizeof(float2) <= TABLE_BYTES, "Q table fits");
 };
 
 
@@ -544,9 +551,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
   char *region = smem;
   float2 *syn_tw = (float2 *)(smem + KS<F, ALG>::REGION);  // exp(+2 pi i j / F), j < F
   float2 *fft_tw = syn_tw + F;                     // exp(-2 pi i j / F), j < F
+  float2 *rot_tw = fft_tw + F;                     // exp(+i pi j (F - 1) / F), j < 2F
   // slot regions 512-byte aligned: TMA destinations (128 B) and the
   // exchange double buffer (aligned to its size, <= 512 B)
-  char *slots_base = (char *)(((uintptr_t)(fft_tw + F) + 511) & ~(uintptr_t)511);
+  char *slots_base = (char *)(((uintptr_t)(rot_tw + 2 * F) + 511) & ~(uintptr_t)511);
   constexpr size_t STG = TMA ? G::STAGE : 0;  // the direct-load variant keeps no staging area
   constexpr size_t slot_bytes = slot_stride<F>(TMA);
 
@@ -569,6 +577,11 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     sincospi(2.0 * j / F, &s, &c);
     syn_tw[j] = make_float2((float)c, (float)s);
     fft_tw[j] = make_float2((float)c, (float)-s);
+  }
+  for (int j = tid; j < 2 * F; j += blockDim.x) {
+    double s, c;
+    sincospi((double)((j * (F - 1)) % (2 * F)) / F, &s, &c);
+    rot_tw[j] = make_float2((float)c, (float)s);
   }
   if constexpr (TMA) {
     if (st == 0) {
@@ -604,6 +617,9 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       __syncthreads();
       loaded = cls;
     }
+    // centred frame: the class's weights are mirror-symmetric and its table
+    // is the real Q (see the iteration section); uniform over the CTA
+    const bool sym = ALG == 0 && F != 128 && a.class_sym && __ldg(a.class_sym + cls);
     const int b = __ldg(a.rounds + (size_t)round * NS + slot);
     if (b < 0) {  // idle this round: keep the slot's prefetch chain going
       if constexpr (TMA) prefetch(round + gridDim.x);
@@ -804,7 +820,12 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 #pragma unroll
       for (int p = 0; p < G::NP; ++p) {
         const int ia = bin_index<F>(w, lane, p, 0), ib = bin_index<F>(w, lane, p, 1);
-        const float2 xa = bin(ia >> G::LOG, ia & (F - 1)), xb = bin(ib >> G::LOG, ib & (F - 1));
+        float2 xa = bin(ia >> G::LOG, ia & (F - 1)), xb = bin(ib >> G::LOG, ib & (F - 1));
+        if (sym) {  // R~[k][l] = R_w[k][l] e^{+i pi (k + l)(F - 1) / F}
+          const float2 ra = rot_tw[(ia >> G::LOG) + (ia & (F - 1))], rb = rot_tw[(ib >> G::LOG) + (ib & (F - 1))];
+          xa = make_float2(xa.x * ra.x - xa.y * ra.y, xa.x * ra.y + xa.y * ra.x);
+          xb = make_float2(xb.x * rb.x - xb.y * rb.y, xb.x * rb.y + xb.y * rb.x);
+        }
         // an arithmetic op gives each SoA pair a fresh, aligned register
         // pair (plain copies let the allocator split the pairs and pay MOVs
         // around every FFMA2 of the hot loop)
@@ -837,7 +858,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     const unsigned kpos = __shfl_sync(0xffffffffu, (unsigned)(rowbase * F) | (unsigned)lane, lane);
     const unsigned tbase =
         __shfl_sync(0xffffffffu, (unsigned)__cvta_generic_to_shared(region), lane);
+
     if constexpr (ALG == 0) {
+    auto iterate = [&](auto symc) {
+    constexpr bool SY = decltype(symc)::value;
 #pragma unroll 1
     for (int it = 0; it < a.iterations; ++it) {
 #if FSE_DIAG & 32
@@ -884,7 +908,67 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       // (from the runtime window size, so that it is not an immediate:
       // ~(F - 1) clears the rank bits, 2 NP <= F)
       const unsigned kmask = PK ? 0u - (unsigned)a.F : 0u;
-      if (!G::PLANAR) {
+      if constexpr (!G::PLANAR && SY) {
+        // Centred frame (mirror-symmetric weights: every interior block).
+        // With w[m][n] = w[F-1-m][n] = w[m][F-1-n], W[k][l] = A(k) A(l) Q(k, l)
+        // with A(k) = e^{-i pi k (F-1)/F} and Q real, anti-periodic
+        // (Q(i + F, j) = -Q(i, j)).  In the frame R~[k][l] = R_w[k][l] /
+        // (A(k) A(l)) the update R_w[k] -= c W[k - (u,v)] becomes
+        // R~[k] -= c~ Q(k - (u,v)), c~ = gamma R~[u,v] / W00, and |R~| = |R_w|:
+        // one real table value per bin (one LDS.64 and two FFMA2 per bin pair
+        // instead of an LDS.128 and four FFMA2).  Entry (i, j) of the table
+        // holds the pair (Q(i, j), Q(i + di, j + dj)), rows / columns from
+        // -(F-1): no wrap arithmetic and no sign flips in the walk.
+#ifndef FSE_PREFETCH
+#define FSE_PREFETCH 2
+#endif
+        constexpr int PD = FSE_PREFETCH;
+        constexpr unsigned RSB = (F == 32 ? 2u : 1u) * (unsigned)G::SYM_C * 8u;  // bytes per pair step
+        // entry of (row rowbase - u, column lane - v): with kpos = rowbase F + lane
+        // and gidx = u F + v, (rowbase - u + F - 1) SYM_C + lane - v + F - 1 =
+        // kpos - gidx + (SYM_C - F)(rowbase - u) + (F - 1)(SYM_C + 1)
+        const unsigned tq =
+            tbase + ((kpos - gidx + (unsigned)(G::SYM_C - F) * ((kpos >> G::LOG) - (gidx >> G::LOG)) +
+                      (unsigned)((F - 1) * (G::SYM_C + 1)))
+                     << 3);
+        float2 qbuf[PD > 0 ? PD : 1];
+#pragma unroll
+        for (int d = 0; d < PD; ++d) qbuf[d] = lds64f(tq + (unsigned)d * RSB);
+#pragma unroll
+        for (int p = 0; p < G::NP; ++p) {
+          FSE_CHECK((tq - tbase) / 8 + (unsigned)p * (RSB / 8) < (unsigned)(G::SYM_R * G::SYM_C));
+          float2 qv;
+          if constexpr (PD > 0) {
+            qv = qbuf[p % PD];
+            if (p + PD < G::NP) qbuf[p % PD] = lds64f(tq + (unsigned)(p + PD) * RSB);
+          } else {
+            qv = lds64f(tq + (unsigned)p * RSB);
+          }
+          ffma2_acc(Rre[p], qv, -cre);
+          ffma2_acc(Rim[p], qv, -cim);
+          float2 mg = fmul2(Rre[p], Rre[p]);
+          mg = ffma2(Rim[p], Rim[p], mg);
+          const int ch = p / (G::NP / CH);
+#if FSE_DIAG & 2
+          bst[ch] = fmax3(bst[ch], mg.x, mg.y);
+#else
+          if constexpr (PK) {
+            const unsigned ka = (__float_as_uint(mg.x) & kmask) | (unsigned)(((G::NP - 1 - p) << 1) | 1);
+            const unsigned kb = (__float_as_uint(mg.y) & kmask) | (unsigned)((G::NP - 1 - p) << 1);
+            bkey = max(bkey, max(ka, kb));
+          } else if constexpr (GM > 0) {
+            gv[2 * (p % GM)] = mg.x;
+            gv[2 * (p % GM) + 1] = mg.y;
+            if (p % GM == GM - 1) {
+              const float t = group_max<GM>(gv);
+              if (t > bst[0]) { bst[0] = t; bg = p / GM; }
+            }
+          } else {
+            first_max(bst[ch], bps[ch], bxs[ch], mg, p);
+          }
+#endif
+        }
+      } else if constexpr (!G::PLANAR) {
         // table index (rowoff, coloff) = ((rowbase - u) mod F, (lane - v) mod F)
         constexpr unsigned RM = (unsigned)(F - 1) << G::LOG;
         const unsigned tp =
@@ -1074,6 +1158,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 #endif
       }
     }
+    };  // iterate
+    // one loop per table kind (a branch inside the loop made ptxas spill)
+    if (sym) iterate(std::integral_constant<bool, !G::PLANAR>{});
+    else iterate(std::false_type{});
     } else {
       // ---------------------------------------- rFSE (rfse.py:69-160)
       // The selection scans the joint projection of every bin onto its
@@ -1214,6 +1302,12 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         cr = ginv * tr.y;
         ci = ginv * tr.z;
         aux = tr.y * tr.y + tr.z * tr.z;
+        if (sym) {  // back from the centred frame: c = c~ e^{-i pi (u + v)(F - 1) / F}
+          const float2 r = rot_tw[(gi >> G::LOG) + (gi & (F - 1))];
+          const float c0 = cr;
+          cr = c0 * r.x + ci * r.y;
+          ci = ci * r.x - c0 * r.y;
+        }
       } else {
         fac = (gi >> 31) ? 1.f : 2.f;
         gi &= 0x7fffffffu;
@@ -1350,7 +1444,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 
 template <int F, int ALG = 0> static size_t fast_smem(int iter_cap) {
   (void)iter_cap;
-  return KS<F, ALG>::REGION + 2 * (size_t)F * sizeof(float2) + 512 +
+  return KS<F, ALG>::REGION + 4 * (size_t)F * sizeof(float2) + 512 +
          KS<F, ALG>::S * slot_stride<F>(true);
 }
 
@@ -1489,6 +1583,34 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
   }
   if (!a.fast_table) return;
   char *tab = (char *)a.fast_table + (size_t)c * a.fast_table_bytes;
+  if (a.sym && a.sym[c]) {
+    // Centred frame (mirror-symmetric weights, see the kernel's iteration
+    // section): Q0[k][l] = W[k][l] e^{+i pi (k + l)(F - 1) / F} is real, and
+    // Q(i, j) = sgn(i) sgn(j) Q0[i mod F][j mod F] for |i|, |j| < F.  Entry
+    // (r, c) = (Q(i, j), Q(i + di, j + dj)), i = r - (F - 1), j = c - (F - 1),
+    // (di, dj) = the offset of member b of a thread's bin pair.
+    for (int i = threadIdx.x; i < FF; i += blockDim.x) {
+      const int k = i / F, l = i - k * F;
+      double sn, cs;
+      sincospi((double)(((k + l) * (F - 1)) % (2 * F)) / F, &sn, &cs);
+      T[i].x = W[i].x * cs - W[i].y * sn;
+    }
+    __syncthreads();
+    auto q = [&](int i, int j) -> float {
+      double sg = 1.0;
+      if (i < 0) { i += F; sg = -sg; } else if (i >= F) { i -= F; sg = -sg; }
+      if (j < 0) { j += F; sg = -sg; } else if (j >= F) { j -= F; sg = -sg; }
+      return (float)(sg * T[i * F + j].x);
+    };
+    const int R = F == 32 ? FG<32>::SYM_R : FG<64>::SYM_R, C = F == 32 ? FG<32>::SYM_C : FG<64>::SYM_C;
+    const int di = F == 32 ? 1 : 0, dj = F == 32 ? 0 : 32;
+    float2 *E = (float2 *)tab;
+    for (int i = threadIdx.x; i < R * C; i += blockDim.x) {
+      const int r = i / C, cc = i - r * C, qi = r - (F - 1), qj = cc - (F - 1);
+      E[i] = make_float2(q(qi, qj), q(qi + di, qj + dj));
+    }
+    return;
+  }
   if (F == 128) {
     const int TR = FG<128>::TROWS;
     float *Tre = (float *)tab, *Tim = Tre + TR * F;

@@ -71,6 +71,8 @@ struct ClassSetupArgs {
   double *tmp;            // n_classes x F x F c128 scratch
   int rfse;               // also build the fused rFSE pair tables (F = 64)
   double *dmin;           // n_classes: min over pair bins of D / W00^2 (rfse only)
+  const int32_t *sym;     // n_classes (may be null): 1 = mirror-symmetric weights, build the
+                          // real centred table Q (fast.cu, "centred frame") instead of W'
 };
 cudaError_t launch_class_setup(const ClassSetupArgs &a, cudaStream_t s);
 
@@ -88,6 +90,7 @@ struct FastArgs {
   size_t table_bytes;
   const float *inv_w00;        // n_classes
   const int32_t *support_rect; // n_classes x 4 (r0, c0, r1, c1) window coords
+  const int32_t *class_sym;    // n_classes (may be null): 1 = the class table is the real centred Q
   const void *frames;
   int dtype;
   long long pitch, frame_stride;
