@@ -401,7 +401,7 @@ int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int 
   std::vector<int32_t> sym(std::max(nc, 1), 0);
   {
     const char *sym_env = getenv("FSE_SYM");
-    const bool allow = p->fast && algorithm == FSE_ALG_CFSE && (F == 32 || F == 64) &&
+    const bool allow = p->fast && algorithm == FSE_ALG_CFSE &&
                        !(sym_env && atoi(sym_env) == 0);
     for (int c = 0; allow && c < nc; ++c) {
       const int8_t *L = labels.data() + (size_t)c * F * F;

@@ -92,11 +92,13 @@ template <int F> struct FG {
   // transforms per lane group and pass: every row pair / column in one pass
   static constexpr int NFT = (F / 2) / (NT / QT);
   static constexpr size_t REGION = TABLE_BYTES;
-  // centred-frame real table (mirror-symmetric classes, F = 32 / 64): SYM_R x
-  // SYM_C float2 entries, rows i = r - (F - 1), columns j = c - (F - 1)
+  // centred-frame real table (mirror-symmetric classes): F = 32 / 64, SYM_R
+  // x SYM_C float2 entries, rows i = r - (F - 1), columns j = c - (F - 1);
+  // F = 128, SYM_R x F floats, columns j mod F (signs in the coefficients)
   static constexpr int SYM_R = F == 32 ? 62 : 2 * F - 1;
-  static constexpr int SYM_C = F == 32 ? 63 : F + 31;
-  static_assert(F == 128 || (size_t)SYM_R * SYM_C * sizeof(float2) <= TABLE_BYTES, "Q table fits");
+  static constexpr int SYM_C = F == 32 ? 63 : F == 64 ? F + 31 : F;
+  static_assert((size_t)SYM_R * SYM_C * (PLANAR ? sizeof(float) : sizeof(float2)) <= TABLE_BYTES,
+                "Q table fits");
 };
 
 
@@ -111,6 +113,15 @@ FSE_DEV void ffma2_acc(float2 &acc, float2 a, float b) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
   unsigned long long bb;
   asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(b));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(x), "l"(bb));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(r));
+}
+// acc = a * b + acc, b a register pair (per-member coefficients)
+FSE_DEV void ffma2_acc2(float2 &acc, float2 a, float2 b) {
+  unsigned long long r, x, bb;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(acc.x), "f"(acc.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(b.x), "f"(b.y));
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(x), "l"(bb));
   asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(r));
 }
@@ -619,7 +630,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     }
     // centred frame: the class's weights are mirror-symmetric and its table
     // is the real Q (see the iteration section); uniform over the CTA
-    const bool sym = ALG == 0 && F != 128 && a.class_sym && __ldg(a.class_sym + cls);
+    const bool sym = ALG == 0 && a.class_sym && __ldg(a.class_sym + cls);
     const int b = __ldg(a.rounds + (size_t)round * NS + slot);
     if (b < 0) {  // idle this round: keep the slot's prefetch chain going
       if constexpr (TMA) prefetch(round + gridDim.x);
@@ -1022,6 +1033,44 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           }
 #endif
         }
+      } else if constexpr (SY) {
+        // centred frame at F = 128: scalar table T[i + F - 1][c] = Q(i, c),
+        // c = (l - v) mod F; the column sign sgn(l - v) of each of the
+        // thread's four columns goes into its coefficient pair
+        const float *Tq = (const float *)region;
+        const int v = (int)(gidx & (F - 1));
+        int co[4];
+        float sg[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          co[h] = (lane + 32 * h - v) & (F - 1);
+          sg[h] = lane + 32 * h < v ? -1.f : 1.f;
+        }
+        const float2 cr2[2] = {make_float2(-cre * sg[0], -cre * sg[1]), make_float2(-cre * sg[2], -cre * sg[3])};
+        const float2 ci2[2] = {make_float2(-cim * sg[0], -cim * sg[1]), make_float2(-cim * sg[2], -cim * sg[3])};
+        const int rq = rowbase - (int)(gidx >> G::LOG) + F - 1;
+#pragma unroll
+        for (int p = 0; p < G::NP; ++p) {
+          const int r = (rq + (p >> 1)) * F;
+          const int q = p & 1;
+          FSE_CHECK(rq + (p >> 1) < G::SYM_R);
+          const float2 qv = make_float2(Tq[r + co[2 * q]], Tq[r + co[2 * q + 1]]);
+          ffma2_acc2(Rre[p], qv, cr2[q]);
+          ffma2_acc2(Rim[p], qv, ci2[q]);
+          float2 mg = fmul2(Rre[p], Rre[p]);
+          mg = ffma2(Rim[p], Rim[p], mg);
+          const int ch = p / (G::NP / CH);
+          if constexpr (GM > 0) {
+            gv[2 * (p % GM)] = mg.x;
+            gv[2 * (p % GM) + 1] = mg.y;
+            if (p % GM == GM - 1) {
+              const float t = group_max<GM>(gv);
+              if (t > bst[0]) { bst[0] = t; bg = p / GM; }
+            }
+          } else {
+            first_max(bst[ch], bps[ch], bxs[ch], mg, p);
+          }
+        }
       } else {
         const float *Tre = (const float *)region;
         const float *Tim = Tre + G::TROWS * F;
@@ -1160,7 +1209,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     }
     };  // iterate
     // one loop per table kind (a branch inside the loop made ptxas spill)
-    if (sym) iterate(std::integral_constant<bool, !G::PLANAR>{});
+    if (sym) iterate(std::true_type{});
     else iterate(std::false_type{});
     } else {
       // ---------------------------------------- rFSE (rfse.py:69-160)
@@ -1602,6 +1651,14 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       if (j < 0) { j += F; sg = -sg; } else if (j >= F) { j -= F; sg = -sg; }
       return (float)(sg * T[i * F + j].x);
     };
+    if (F == 128) {
+      float *Tq = (float *)tab;
+      for (int i = threadIdx.x; i < FG<128>::SYM_R * F; i += blockDim.x) {
+        const int r = i / F, cc = i - r * F;
+        Tq[i] = q(r - (F - 1), cc);
+      }
+      return;
+    }
     const int R = F == 32 ? FG<32>::SYM_R : FG<64>::SYM_R, C = F == 32 ? FG<32>::SYM_C : FG<64>::SYM_C;
     const int di = F == 32 ? 1 : 0, dj = F == 32 ? 0 : 32;
     float2 *E = (float2 *)tab;
