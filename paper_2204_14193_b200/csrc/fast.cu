@@ -34,7 +34,7 @@
 //   FSE_PREFETCH            W' loads issued this many pairs ahead (2)
 //   FSE_CHAINS64 / FSE_CHAINS128  independent first-max chains (1 / 1)
 //   FSE_XTREE               F=128 warp-candidate merge in registers (1)
-//   FSE_MAX3 / FSE_PACKKEY  alternative first-max trackers (0 / 0)
+//   FSE_MAX3 / FSE_PACKKEY  alternative first-max trackers (1 / 0)
 //   FSE_DIAG                diagnostic builds (bit 32: per-phase clock probe)
 //   FSE_CHECKS              device asserts on every shared/global index
 #include <stdlib.h>
@@ -143,7 +143,10 @@ FSE_DEV float fmax3(float a, float b, float c) {
   return r;
 }
 #ifndef FSE_MAX3
-#define FSE_MAX3 0  // FMNMX3 running maximum: one op fewer per pair, measured -3 % (F=64)
+// FMNMX3 running maximum: one op fewer per pair and one op on the loop-carried
+// chain.  With the complex-table loop it measured -3 % (F=64); with the
+// centred-frame loop +1.7 % (config 5), +3.6 % (F=32), +-0 (F=128)
+#define FSE_MAX3 1
 #endif
 // first-max tracker step over bin pair p with |R|^2 = (mg.x, mg.y): the
 // larger value strictly above the running maximum wins, member a on equal

@@ -612,3 +612,32 @@ def test_concealer_graph_replay(fse):
     b = replay(copy=True)
     assert not np.array_equal(a, b)
     assert np.array_equal(b, con.run(con.pin(frames2), copy=True))
+
+
+@pytest.mark.parametrize("F,B,border", [(32, 8, 8), (64, 16, 16), (128, 32, 16)])
+def test_centred_frame_and_complex_table_paths(fse, F, B, border, monkeypatch):
+    """Mirror-symmetric (unclipped) classes iterate in the centred frame (real
+    table, fast.cu); FSE_SYM=0 keeps them on the complex W' table.  Both
+    paths pass the fp32 oracle gate on the same blocks, the plan reports the
+    centred classes, and the two tile sets agree to fp32 noise."""
+    from paper_2204_14193_b200.synth import field
+    imgs = np.stack([field(512, 512, seed=60 + k) for k in range(2)]).astype(np.float32)
+    blocks = np.array([(f, 2 * B * i, 2 * B * j) for f in range(2) for i in range(256 // B)
+                       for j in range(256 // B)], np.int32)  # edge rows / columns clip
+    out = {}
+    for mode in ("centred", "complex"):
+        if mode == "complex":
+            monkeypatch.setenv("FSE_SYM", "0")
+        tiles, get, plan = _run_plan(fse, imgs, blocks, F, B, border, 100)
+        info = plan.info
+        assert info["fast_path"] == 1
+        if mode == "centred":
+            assert 1 <= info["n_centred"] < info["n_classes"]
+        else:
+            assert info["n_centred"] == 0
+        st = fp32_gate(imgs, blocks, tiles, get, F, B, border, 0.8, 0.5, 100,
+                       truth=_truth(imgs, blocks, B), log=f"paths_{mode}_F{F}")
+        out[mode] = tiles
+        print(mode, F, {k: v for k, v in st.items() if k != "outliers"})
+    d = np.abs(out["centred"].astype(np.float64) - out["complex"])
+    assert np.median(d) < 0.5 and np.mean(d) < 0.5
