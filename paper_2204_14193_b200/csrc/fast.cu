@@ -33,7 +33,7 @@
 //   FSE_SLOTS64 / FSE_SLOTS32  blocks per CTA at F=64 / 32 (6 / 20)
 //   FSE_PREFETCH            W' loads issued this many pairs ahead (2)
 //   FSE_CHAINS64 / FSE_CHAINS128  independent first-max chains (1 / 1)
-//   FSE_XTREE               F=128 warp-candidate merge in registers (1)
+//   FSE_XTREE               F=128 warp-candidate merge in registers (0)
 //   FSE_MAX3 / FSE_PACKKEY  alternative first-max trackers (1 / 0)
 //   FSE_DIAG                diagnostic builds (bit 32: per-phase clock probe)
 //   FSE_CHECKS              device asserts on every shared/global index
@@ -889,7 +889,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       // (shorter dependent compare/select chains), merged in order below;
       // measured best: 1 (2 helped the 32-bins-per-thread F = 64 variant)
 #ifndef FSE_XTREE
-#define FSE_XTREE 1  // F=128: register merge of the 8 warp candidates (+0.6 %)
+// F=128 warp-candidate merge: 1 = every lane reads all 8 candidates and
+// merges in registers (+0.6 % with the complex-table loop), 0 = one REDUX
+// pair over a lane-per-warp load (+4.8 % with the centred-frame loop)
+#define FSE_XTREE 0
 #endif
 #ifndef FSE_CHAINS128
 #define FSE_CHAINS128 1
