@@ -366,12 +366,22 @@ def main():
     from paper_2204_14193_b200 import sharding
     from paper_2204_14193_b200.synth import field_torch
 
-    torch.cuda.set_device(local)
+    # FSE_BENCH_SHARE_GPU=1: a functional check of the N-rank flow on a box
+    # with fewer GPUs (ranks share devices round-robin, gloo for the barriers
+    # and the max-over-ranks reduction); its numbers are not scaling numbers
+    share = os.environ.get("FSE_BENCH_SHARE_GPU") == "1"
+    dev_index = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(dev_index)
     dist = None
+    red_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+            red_dev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     all_blocks = fse.frames_pattern(cfg["frames"], cfg["H"], cfg["W"], cfg["B"], cfg["frac"],
                                     SEED if a.config == "5" else 3)
     sh = sharding.shard_blocks(all_blocks, cfg["frames"], rank, world)
@@ -404,7 +414,7 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
@@ -420,7 +430,7 @@ def main():
         dist.barrier()
     elapsed_ms = t0.elapsed_time(t1)
     kern_ms = [s.elapsed_time(e) for s, e in ev]
-    mx = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    mx = torch.tensor([elapsed_ms], dtype=torch.float64, device=red_dev)
     if dist:
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     elapsed_ms = float(mx.item())
@@ -447,7 +457,7 @@ def main():
         t = time.perf_counter()
         for _ in range(a.steps):
             con.run(host, out=host_slice)
-        et = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device="cuda")
+        et = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=red_dev)
         if dist:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": total_blocks * a.steps / float(et.item()), "unit": "blocks/s",
@@ -479,7 +489,7 @@ def main():
     # roofline of the dominant kernel (the fused kernel is the only launch per step)
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    sms = torch.cuda.get_device_properties(dev_index).multi_processor_count
     F, I = cfg["F"], cfg["iters"]
     smem_bytes_blk = 8.0 * F * F * I  # W' read per bin-iteration
     flops_blk = 11.0 * F * F * I
@@ -504,7 +514,8 @@ def main():
                              "the timed region)") if a.tiles == "host" else
                             "device tiles, one D2H into the shared host buffer at the end of the timed region",
                    "plan": plan.info},
-        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_smem, "unit": "TB/s",
+        "roofline": {"bound": "smem", "scope": "per GPU: rank 0's blocks / its kernel time",
+                     "achieved": achieved, "peak": peak_smem, "unit": "TB/s",
                      "frac": achieved / peak_smem,
                      "traffic": (nt["dram_bytes_per_block"] * len(blocks)) if nt.get("dram_bytes_per_block") else None,
                      "traffic_source": nt.get("source"),
@@ -523,6 +534,9 @@ def main():
         "gather": {"buffer": "one /dev/shm mapping, page-locked by every rank", "bytes": int(gbuf.nbytes),
                    "last_block_nonzero": gathered_ok},
     }
+    if share:
+        line["shared_gpus"] = (f"FSE_BENCH_SHARE_GPU: {world} ranks on {torch.cuda.device_count()} device(s); "
+                               "a functional check of the N-rank flow, not a scaling number")
     if e2e:
         line["e2e"] = e2e
     if parity:
