@@ -528,7 +528,14 @@ def main():
                      "measured_ceilings": ceil,
                      "frac_of_measured_lds128": achieved / ceil["lds128_TBps"] if ceil else None,
                      "frac_of_loop_mix_ceiling": achieved / ceil["loop_mix_TBps"] if ceil else None,
-                     "kernel_ms": statistics.mean(kern_ms)},
+                     "kernel_ms": statistics.mean(kern_ms),
+                     "algorithmic_smem_bytes_per_block": smem_bytes_blk,
+                     "kernel_scan_smem_bytes_per_block": {
+                         "centred_classes": 4.0 * F * F * I, "other_classes": smem_bytes_blk},
+                     "note": ("achieved counts the algorithm's W' traffic (8 B per bin-iteration, SURVEY 8(d)); "
+                              "the kernel's centred-frame loop reads a real table, 4 B per bin-iteration, for "
+                              "mirror-symmetric (interior) classes, so the shared-memory pipe itself runs at "
+                              "about half this rate and the loop is issue/latency-bound (DESIGN 4.1)")},
         "clocks": clocks,
         "gpu_launches": a.steps * 1,
         "gather": {"buffer": "one /dev/shm mapping, page-locked by every rank", "bytes": int(gbuf.nbytes),
