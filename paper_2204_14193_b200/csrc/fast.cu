@@ -201,17 +201,31 @@ FSE_DEV float4 lds128f(unsigned addr) {
 // a = R_w[k]:  crit = A a.re^2 + C a.im^2 - D a.re a.im  (rfse.py:86-111).
 // F = 32: sixteen one-warp blocks per CTA (the rFSE loop state needs up to
 // 128 registers), tables for bins (2p, c), (2p + 1, c) of pair p, column c.
-template <int F> constexpr int rf_slots() { return F == 32 ? 16 : 4; }
-// pair-criterion tables: F^2 / 2 bin pairs x (float4 + float2)
+// F = 128: one block per CTA in the centred frame only (mirror-symmetric
+// classes; rFSE plans send clipped classes to the per-window kernel).  Its
+// pair criterion there needs two real coefficients per bin, alpha and beta
+// (below), which depend on the doubled frequency only: a 64 x 32 x 2 table
+// (32 KB) that each block copies into its FFT scratch after the setup
+// (the Q table leaves no room for it in the class region).
+template <int F> constexpr int rf_slots() { return F == 32 ? 16 : F == 64 ? 4 : 1; }
+// pair-criterion tables: F^2 / 2 bin pairs x (float4 + float2); F = 128 the
+// centred alpha | beta halves, 64 doubled rows x 32 lanes x float2 each
 template <int F> constexpr size_t rf_t2_bytes() {
-  return (size_t)F * F / 2 * (sizeof(float4) + sizeof(float2));
+  return F == 128 ? (size_t)2 * 64 * 32 * sizeof(float2)
+                  : (size_t)F * F / 2 * (sizeof(float4) + sizeof(float2));
 }
 template <int F, int ALG> struct KS {  // per-algorithm launch shape
   static constexpr int S = ALG ? rf_slots<F>() : FG<F>::S;
   static constexpr int CTA = FG<F>::NT * S;
-  static constexpr size_t REGION = ALG ? FG<F>::TABLE_BYTES + rf_t2_bytes<F>() : FG<F>::REGION;
+  static constexpr size_t REGION =
+      ALG && F != 128 ? FG<F>::TABLE_BYTES + rf_t2_bytes<F>() : FG<F>::REGION;
 };
 
+FSE_DEV float lds32f(unsigned addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
 FSE_DEV float2 lds64f(unsigned addr) {
   float2 v;
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
@@ -559,7 +573,7 @@ template <int F, bool TMA, int ALG>
 __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     fast_kernel(FastArgs a, int iter_cap, const __grid_constant__ CUtensorMap tmap) {
   typedef FG<F> G;
-  static_assert(ALG == 0 || F == 32 || F == 64, "the fused rFSE kernel is built for F = 32, 64");
+  static_assert(ALG == 0 || F == 32 || F == 64 || F == 128, "fused window sizes");
   constexpr int NS = KS<F, ALG>::S;  // blocks (slots) per CTA
   extern __shared__ __align__(16) char smem[];
   char *region = smem;
@@ -626,14 +640,17 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     const int cls = __ldg(a.round_class + round);
     if (cls != loaded) {
       __syncthreads();
-      copy_table(region, (const char *)a.table + (size_t)cls * a.table_bytes, a.table_bytes, tid,
+      // (rFSE at F = 128: the Q table only; the criterion table goes to the
+      // scratch per block)
+      copy_table(region, (const char *)a.table + (size_t)cls * a.table_bytes,
+                 ALG && F == 128 ? (size_t)G::SYM_R * F * sizeof(float) : a.table_bytes, tid,
                  blockDim.x);
       __syncthreads();
       loaded = cls;
     }
     // centred frame: the class's weights are mirror-symmetric and its table
     // is the real Q (see the iteration section); uniform over the CTA
-    const bool sym = ALG == 0 && a.class_sym && __ldg(a.class_sym + cls);
+    const bool sym = (ALG == 0 || F == 128) && a.class_sym && __ldg(a.class_sym + cls);
     const int b = __ldg(a.rounds + (size_t)round * NS + slot);
     if (b < 0) {  // idle this round: keep the slot's prefetch chain going
       if constexpr (TMA) prefetch(round + gridDim.x);
@@ -1217,6 +1234,146 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     // one loop per table kind (a branch inside the loop made ptxas spill)
     if (sym) iterate(std::true_type{});
     else iterate(std::false_type{});
+    } else if constexpr (F == 128) {
+      // ------------------------- rFSE at F = 128 in the centred frame
+      // (interior classes; rfse.py:69-160).  With R~ = R_w / phi (phi(k) =
+      // A(k) A(l), see the cFSE centred loop) and W[2k] = phi(k)^2 Q(2k), the
+      // pair criterion 2 (p.re a.re + p.im a.im) of rfse.py:93-103 is
+      //   crit = alpha R~.re^2 + beta R~.im^2,
+      //   alpha = 2 / (W00 + Q(2k)), beta = 2 / (W00 - Q(2k)),
+      // the joint projection is p~ = (R~.re / (W00 + Q2), R~.im / (W00 - Q2))
+      // = (alpha, beta) R~ / 2, and the pair update R_w -= c W[k - s] +
+      // conj(c) W[k - m] (m the mirror bin) becomes R~ -= c~ Q(k - s) +
+      // sg conj(c~) Q(k - m) with c~ = gamma p~ (c = c~ phi(s), restored
+      // after the loop) and the sign sg below.  A
+      // self-conjugate bin (2k = 0 mod F: s in {0, F/2}^2, phi(s) in {1, i,
+      // -1}) has crit = a.re^2 / W00 with a = phi R~: (alpha, beta) = (1/W00,
+      // 0) for real phi, (0, 1/W00) for imaginary phi, p~ = (alpha, beta) R~.
+      // alpha and beta depend on (2k mod F, 2l mod F): the table holds them
+      // at the doubled row 2 r2 (r2 < 64) and the lane's doubled columns
+      // (2 lane, 2 lane + 64); a doubled row or column that wraps past F
+      // flips the sign of Q(2k), i.e. swaps alpha and beta.
+      const unsigned crit_base = smem_u32(sp.scratch) + (unsigned)(G::SCRATCH - rf_t2_bytes<F>());
+      {
+        const char *src = (const char *)a.table + (size_t)cls * a.table_bytes + G::TABLE_BYTES;
+        for (int i = st; i < (int)(rf_t2_bytes<F>() / 16); i += G::NT)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(crit_base + 16u * (unsigned)i),
+                       "l"(src + 16 * (size_t)i)
+                       : "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        slot_sync<F>(slot);
+      }
+      constexpr unsigned HALF = (unsigned)(rf_t2_bytes<F>() / 2);  // alpha half | beta half
+      // this warp's entries: doubled row of row r = rowbase + rr is (r mod 64)
+      // (rows >= 64 wrap: alpha <-> beta); pair p = 2 rr + q, q = 1 for the
+      // lane's columns + 64 (their doubled columns wrap: swap again)
+      const unsigned cw = __shfl_sync(0xffffffffu, crit_base + (unsigned)((((rowbase & 63) * 32) + lane) * 8), lane);
+      const unsigned pA = w >= 4 ? cw + HALF : cw, pB = w >= 4 ? cw : cw + HALF;
+      const float *Tq = (const float *)region;
+      unsigned midx = 0;             // bin of the previous pick's second atom
+      float c2re = 0.f, c2im = 0.f;  // its coefficient (conj c~, or 0 after a self-conjugate pick)
+      int tally = 0;
+      nit = 0;
+#pragma unroll 1
+      for (int it = 0; it < a.iterations && tally < a.stop_tally; ++it) {
+        const int v1 = (int)(gidx & (F - 1)), v2 = (int)(midx & (F - 1));
+        int co1[4], co2[4];
+        float s1[4], s2[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          co1[h] = (lane + 32 * h - v1) & (F - 1);
+          co2[h] = (lane + 32 * h - v2) & (F - 1);
+          s1[h] = lane + 32 * h < v1 ? -1.f : 1.f;
+          s2[h] = lane + 32 * h < v2 ? -1.f : 1.f;
+        }
+        const float2 a1r[2] = {make_float2(-cre * s1[0], -cre * s1[1]), make_float2(-cre * s1[2], -cre * s1[3])};
+        const float2 a1i[2] = {make_float2(-cim * s1[0], -cim * s1[1]), make_float2(-cim * s1[2], -cim * s1[3])};
+        const float2 a2r[2] = {make_float2(-c2re * s2[0], -c2re * s2[1]), make_float2(-c2re * s2[2], -c2re * s2[3])};
+        const float2 a2i[2] = {make_float2(-c2im * s2[0], -c2im * s2[1]), make_float2(-c2im * s2[2], -c2im * s2[3])};
+        const int rq1 = rowbase - (int)(gidx >> G::LOG) + F - 1, rq2 = rowbase - (int)(midx >> G::LOG) + F - 1;
+        float bst = -1.f, bxs = 0.f;
+        int bps = 0;
+        float2 xa = make_float2(0.f, 0.f), xb = xa;
+#pragma unroll
+        for (int p = 0; p < G::NP; ++p) {
+          const int q = p & 1, rr = p >> 1;
+          const int r1 = (rq1 + rr) * F, r2 = (rq2 + rr) * F;
+          FSE_CHECK(rq1 + rr < G::SYM_R && rq2 + rr < G::SYM_R);
+          const float2 q1 = make_float2(Tq[r1 + co1[2 * q]], Tq[r1 + co1[2 * q + 1]]);
+          const float2 q2 = make_float2(Tq[r2 + co2[2 * q]], Tq[r2 + co2[2 * q + 1]]);
+          ffma2_acc2(Rre[p], q1, a1r[q]);
+          ffma2_acc2(Rim[p], q1, a1i[q]);
+          ffma2_acc2(Rre[p], q2, a2r[q]);
+          ffma2_acc2(Rim[p], q2, a2i[q]);
+          if (q == 0) {
+            xa = lds64f(pA + (unsigned)(rr * 256));
+            xb = lds64f(pB + (unsigned)(rr * 256));
+          }
+          const float2 al = q ? xb : xa, be = q ? xa : xb;
+          const float2 t1 = fmul2(al, Rre[p]), t2 = fmul2(be, Rim[p]);
+          float2 cr = fmul2(t1, Rre[p]);
+          cr = ffma2(t2, Rim[p], cr);
+          first_max(bst, bps, bxs, cr, p);
+        }
+        const int myidx = bin_index<F>(w, lane, bps, bxs >= bst ? 0 : 1);
+        const unsigned key = __float_as_uint(fmaxf(bst, 0.f));  // crit >= 0: monotone as unsigned
+        const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
+        const unsigned widx = __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
+        int pw, mw, ow;
+        decode_bin<F>((int)widx, w, pw, mw, ow);
+        float are, aim;
+        pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
+        are = __shfl_sync(0xffffffffu, are, ow);
+        aim = __shfl_sync(0xffffffffu, aim, ow);
+        // the 8 warp candidates: (crit, index) max, first index on ties
+        if (lane == 0) sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
+        slot_sync<F>(slot);
+        const uint4 cnd = lane < G::NW ? lds128u(xc + 16u * lane) : make_uint4(0u, 0xffffffffu, 0u, 0u);
+        const unsigned gkey = __reduce_max_sync(0xffffffffu, cnd.x);
+        gidx = __reduce_min_sync(0xffffffffu, cnd.x == gkey ? cnd.y : 0xffffffffu);
+        const int wl = (int)(gidx / (unsigned)(G::RPW * F));
+        are = __shfl_sync(0xffffffffu, __uint_as_float(cnd.z), wl);
+        aim = __shfl_sync(0xffffffffu, __uint_as_float(cnd.w), wl);
+        xc ^= (unsigned)(G::NW * sizeof(uint4));
+        // joint projection of the chosen bin from its (alpha, beta)
+        const unsigned u = gidx >> G::LOG, v = gidx & (F - 1);
+        const bool self = ((2 * u) & (F - 1)) == 0 && ((2 * v) & (F - 1)) == 0;
+        const unsigned ea = crit_base + (((u & 63u) * 32u + (v & 31u)) * 8u) + ((v >> 5) & 1u) * 4u;
+        float al = lds32f(ea), be = lds32f(ea + HALF);
+        if ((u >= 64u) != (((v >> 6) & 1u) != 0u)) {
+          const float t = al;
+          al = be;
+          be = t;
+        }
+        const float fac = self ? 1.f : 0.5f;
+        float pr = fac * al * are, pi = fac * be * aim;
+        // The mirror member m = (-u, -v) mod F: conj(phi(m)) = sg phi(s) with
+        // sg = (-1)^([u != 0] + [v != 0]) (A(F - x) = -conj(A(x))), so its
+        // centred projection is sg conj(p~) and the second atom, read at the
+        // shift m, carries sg conj(c~).  The pair is represented by its
+        // smaller row-major member (rfse.py:113-121).
+        const float sg = ((u != 0u) != (v != 0u)) ? -1.f : 1.f;
+        unsigned mi = (((F - u) & (F - 1)) << G::LOG) | ((F - v) & (F - 1));
+        if (!self && mi < gidx) {
+          const unsigned t = gidx;
+          gidx = mi;
+          mi = t;
+          pr = sg * pr;
+          pi = -sg * pi;
+        }
+        midx = self ? gidx : mi;
+        cre = a.gamma * pr;
+        cim = a.gamma * pi;
+        c2re = self ? 0.f : sg * cre;
+        c2im = self ? 0.f : -sg * cim;
+        tally += self ? 1 : 2;
+        if (st == 0) {
+          FSE_CHECK(a.trace_scratch || (unsigned)it * 16u < (unsigned)(G::SCRATCH - rf_t2_bytes<F>()));
+          sp.trace[it] = make_float4(__uint_as_float(gidx | (self ? 0x80000000u : 0u)), cre, cim,
+                                     __uint_as_float(gkey));
+        }
+        nit = it + 1;
+      }
     } else {
       // ---------------------------------------- rFSE (rfse.py:69-160)
       // The selection scans the joint projection of every bin onto its
@@ -1369,6 +1526,12 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         cr = tr.y;
         ci = tr.z;
         aux = __uint_as_float(__float_as_uint(tr.w));
+        if (sym) {  // back from the centred frame: c = c~ phi(u, v)
+          const float2 r = rot_tw[(gi >> G::LOG) + (gi & (F - 1))];
+          const float c0 = cr;
+          cr = c0 * r.x + ci * r.y;
+          ci = ci * r.x - c0 * r.y;
+        }
       }
       const unsigned tu = gi >> G::LOG;
       sp.trace[k] = make_float4(__uint_as_float(tu | ((gi & (F - 1)) << 16)), cr, ci, aux);
@@ -1506,17 +1669,20 @@ template <int F, int ALG = 0> static size_t fast_smem(int iter_cap) {
 bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algorithm) {
   size_t smem, tb;
   int S;
-  if (algorithm == 1) {  // fused rFSE: F = 32, 64
-    if (F != 32 && F != 64) return false;
-    cfg->global_trace = iterations > (F == 32 ? FG<32>::TRACE_CAP : FG<64>::TRACE_CAP);
-    smem = F == 32 ? fast_smem<32, 1>(0) : fast_smem<64, 1>(0);
+  if (algorithm == 1) {  // fused rFSE: F = 32, 64; F = 128 centred-frame classes only
+    if (F != 32 && F != 64 && F != 128) return false;
+    cfg->global_trace = iterations > (F == 32   ? FG<32>::TRACE_CAP
+                                      : F == 64 ? FG<64>::TRACE_CAP
+                                                : FG<128>::TRACE_CAP);
+    smem = F == 32 ? fast_smem<32, 1>(0) : F == 64 ? fast_smem<64, 1>(0) : fast_smem<128, 1>(0);
     if (smem > 227 * 1024) return false;
-    cfg->slots = F == 32 ? rf_slots<32>() : rf_slots<64>();
-    cfg->threads = F == 32 ? KS<32, 1>::CTA : KS<64, 1>::CTA;
+    cfg->slots = F == 32 ? rf_slots<32>() : F == 64 ? rf_slots<64>() : rf_slots<128>();
+    cfg->threads = F == 32 ? KS<32, 1>::CTA : F == 64 ? KS<64, 1>::CTA : KS<128, 1>::CTA;
     cfg->smem_bytes = (int)smem;
     cfg->grid = sm_count;
-    cfg->table_bytes = F == 32 ? FG<32>::TABLE_BYTES + rf_t2_bytes<32>()
-                               : FG<64>::TABLE_BYTES + rf_t2_bytes<64>();
+    cfg->table_bytes = F == 32   ? FG<32>::TABLE_BYTES + rf_t2_bytes<32>()
+                       : F == 64 ? FG<64>::TABLE_BYTES + rf_t2_bytes<64>()
+                                 : FG<128>::TABLE_BYTES + rf_t2_bytes<128>();
     return true;
   }
   switch (F) {
@@ -1562,9 +1728,10 @@ template <int F, int ALG> static cudaError_t launch_fast_t(const FastArgs &a, co
 cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap,
                         cudaStream_t s) {
   if (a.algorithm == 1)
-    return a.F == 64   ? launch_fast_t<64, 1>(a, cfg, tmap, s)
-           : a.F == 32 ? launch_fast_t<32, 1>(a, cfg, tmap, s)
-                       : cudaErrorInvalidValue;
+    return a.F == 64    ? launch_fast_t<64, 1>(a, cfg, tmap, s)
+           : a.F == 32  ? launch_fast_t<32, 1>(a, cfg, tmap, s)
+           : a.F == 128 ? launch_fast_t<128, 1>(a, cfg, tmap, s)
+                        : cudaErrorInvalidValue;
   switch (a.F) {
     case 32: return launch_fast_t<32, 0>(a, cfg, tmap, s);
     case 64: return launch_fast_t<64, 0>(a, cfg, tmap, s);
@@ -1662,6 +1829,31 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       for (int i = threadIdx.x; i < FG<128>::SYM_R * F; i += blockDim.x) {
         const int r = i / F, cc = i - r * F;
         Tq[i] = q(r - (F - 1), cc);
+      }
+      if (a.rfse) {
+        // centred rFSE criterion table (the kernel's F = 128 rFSE loop):
+        // alpha = 2 / (W00 + Q0), beta = 2 / (W00 - Q0) at the doubled
+        // frequency (2 r2, 2 lane + 64 h); (1 / W00, 0) at (0, 0), the
+        // self-conjugate bins.  alpha half, then beta half.
+        const double w00 = W[0].x;
+        float2 *CA = (float2 *)(tab + FG<128>::TABLE_BYTES), *CB = CA + 64 * 32;
+        for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
+          const int r2 = i >> 5, ln = i & 31;
+          double al[2], be[2];
+          for (int h = 0; h < 2; ++h) {
+            const int k2 = 2 * r2, l2 = 2 * ln + 64 * h;
+            const double q0 = T[k2 * F + l2].x;
+            if (k2 == 0 && l2 == 0) {
+              al[h] = 1.0 / w00;
+              be[h] = 0.0;
+            } else {
+              al[h] = 2.0 / (w00 + q0);
+              be[h] = 2.0 / (w00 - q0);
+            }
+          }
+          CA[i] = make_float2((float)al[0], (float)al[1]);
+          CB[i] = make_float2((float)be[0], (float)be[1]);
+        }
       }
       return;
     }

@@ -1,5 +1,8 @@
 """Fused rFSE vs fused cFSE throughput on config-5 frames at equal basis-function
-counts (cFSE: I = BF iterations; rFSE: basis_target = BF)."""
+counts (cFSE: I = BF iterations; rFSE: basis_target = BF).
+Usage: python scripts/rfse_rate.py [F]  (F = 32, 64, 128; F = 128 uses the
+config-4b geometry, border 16, 4 % loss: interior blocks fused, clipped ones
+per window, both inside the timed plan run)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -7,12 +10,13 @@ import paper_2204_14193_b200 as fse
 from paper_2204_14193_b200.synth import field_torch
 F = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 nf = 32 if F == 64 else 8
+border = 16 if F == 128 else F // 4
 frames = field_torch(nf, 2160, 3840, seed=5, device="cuda", edges=True)
-blocks = fse.frames_pattern(nf, 2160, 3840, F // 4, 0.05, seed=5)
+blocks = fse.frames_pattern(nf, 2160, 3840, F // 4, 0.04 if F == 128 else 0.05, seed=5)
 for bf in (100, 200):
     for alg in ("cfse", "rfse"):
         kw = dict(iterations=bf) if alg == "cfse" else dict(iterations=bf, basis_target=bf)
-        plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(F // 4, F // 4, F), rho_hat=0.8, gamma=0.5,
+        plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(F // 4, border, F), rho_hat=0.8, gamma=0.5,
                                algorithm=alg, **kw)
         t = plan.run(frames)
         torch.cuda.synchronize()

@@ -119,7 +119,7 @@ def _trace_getter(tr32):
     return get
 
 
-def _rfse_gate(fse, img, blocks, t32, tr32, t64, F, B, iters, bt, log=None):
+def _rfse_gate(fse, img, blocks, t32, tr32, t64, F, B, iters, bt, log=None, border=None):
     """fp32 rFSE gate against the independent C oracle's rFSE (oracle/gate.py
     rfse_gate, rfse.py:37-210 restated): every block within 0.5 gray levels
     except certified near-ties (criterion gap < 1e-6 relative, or within
@@ -129,9 +129,11 @@ def _rfse_gate(fse, img, blocks, t32, tr32, t64, F, B, iters, bt, log=None):
     from oracle.gate import rfse_gate
     fr = img.cpu().numpy() if hasattr(img, "cpu") else np.asarray(img)
     fr = fr if fr.ndim == 3 else fr[None]
-    st = rfse_gate(fr, blocks, t32.cpu().numpy(), _trace_getter(tr32), F, B, B, 0.8, 0.5, iters, bt, log=log)
+    border = B if border is None else border
+    st = rfse_gate(fr, blocks, t32.cpu().numpy(), _trace_getter(tr32), F, B, border, 0.8, 0.5, iters, bt,
+                   log=log)
     if t64 is not None:
-        ref = orc.conceal_blocks_rfse(fr, blocks, B, B, F, 0.8, 0.5, iters, bt)
+        ref = orc.conceal_blocks_rfse(fr, blocks, B, border, F, 0.8, 0.5, iters, bt)
         np.testing.assert_allclose(t64.cpu().numpy(), ref, rtol=0, atol=1e-9)
     return {k: v for k, v in st.items() if k != "outliers"}
 
@@ -350,3 +352,90 @@ def test_fused_rfse_on_a_config_frame(fse, F):
     t32, tr = plan.run(frames, tile_dtype="f32", trace=True)
     st = _rfse_gate(fse, frames, blocks, t32, tr, None, F, B, iters, bt, log=f"rfse{F}_config_frame")
     print(F, st)
+
+
+# ---------------------------------------------------------------- F = 128
+
+
+@pytest.mark.parametrize("dtype,iters,bt", [("u8", 60, None), ("f32", 100, 100)])
+def test_fused_rfse128_split_plan(fse, dtype, iters, bt):
+    """F = 128 rFSE: interior blocks run the fused centred-frame kernel, the
+    clipped corner/edge blocks the per-window kernel (split plan, tiles and
+    traces scattered back to their positions).  Gate against the C oracle's
+    rFSE: every block within 0.5 gray levels except certified near-ties;
+    canonical members and the tally rule."""
+    import torch
+    from paper_2204_14193_b200.synth import field_torch
+    H, W = 384, 544
+    frames = field_torch(2, H, W, seed=29, device="cuda", edges=True)
+    if dtype != "u8":
+        frames = frames.to(torch.float32)
+    interior = [[f, 64 + 96 * i, 64 + 112 * j] for f in range(2) for i in range(3) for j in range(4)]
+    clipped = [[0, 0, 0], [0, 0, W - 32], [1, H - 32, 0], [1, H - 32, W - 32], [0, 20, 250], [1, 200, 8]]
+    blocks = np.array(interior[:10] + clipped + interior[10:], np.int32)
+    kw = dict(iterations=iters) if bt is None else dict(iterations=iters, basis_target=bt)
+    plan = fse.ConcealPlan(blocks, H, W, fse.Geometry(32, 16, 128), rho_hat=0.8, gamma=0.5,
+                           algorithm="rfse", precision="fp32", **kw)
+    assert plan.info["fast_path"] == 1 and plan.info["n_centred"] == 1
+    t32, tr = plan.run(frames, tile_dtype="f32", trace=True)
+    print(_rfse_gate(fse, frames, blocks, t32, tr, None, 128, 32, iters, bt,
+                     log=f"rfse128_{dtype}_{iters}_{bt}", border=16))
+    uv = tr["uv"].cpu().numpy()
+    for k in range(len(blocks)):
+        used = uv[k, :, 0] >= 0
+        u, v = uv[k, used, 0], uv[k, used, 1]
+        mu, mv = (-u) % 128, (-v) % 128
+        assert np.all(u * 128 + v <= mu * 128 + mv)
+        selfc = ((2 * u) % 128 == 0) & ((2 * v) % 128 == 0)
+        tally = int(np.sum(np.where(selfc, 1, 2)))
+        if bt is None:
+            assert used.sum() == plan.iterations
+        else:
+            assert tally >= bt and tally - (1 if selfc[-1] else 2) < bt
+
+
+def test_fused_rfse128_selection_sequence(fse):
+    """The fused F = 128 centred-frame rFSE picks the C oracle's canonical
+    pair sequence over all 60 iterations, up to a certified near-tie."""
+    import torch
+    from paper_2204_14193_b200.synth import frame_u8
+    from tests._windows import window_of
+    fr = frame_u8(384, 512, seed=5)
+    blocks = np.array([[0, 64 + 64 * i, 64 + 96 * j] for i in range(4) for j in range(4)], np.int32)
+    plan = fse.ConcealPlan(blocks, 384, 512, fse.Geometry(32, 16, 128), rho_hat=0.8, gamma=0.5,
+                           algorithm="rfse", precision="fp32", iterations=60)
+    assert plan.info["fast_path"] == 1
+    _, tr = plan.run(torch.from_numpy(fr).cuda(), tile_dtype="f32", trace=True)
+    get = _trace_getter(tr)
+    from oracle import oracle as orc
+    from oracle.gate import first_rfse_divergence
+    full, ties = 0, []
+    for k, (f, t, l) in enumerate(blocks):
+        s, lab = window_of(fr.astype(np.float64), t, l, 128, 32, 16)
+        o = orc.extrapolate_rfse(s, lab, 0.8, 0.5, 60)
+        at = first_rfse_divergence((o["us"], o["vs"]), get(k))
+        if at is None:
+            full += 1
+            continue
+        cert = orc.rfse_divergence_certificate(s, lab, 0.8, 0.5, at, get(k))
+        assert cert["strict"] or cert["bounded"], (k, cert)
+        ties.append((k, cert))
+    print("identical", full, "certified ties", ties)
+    assert full >= len(blocks) // 2
+
+
+def test_fused_rfse128_config4b(fse):
+    """Config 4b geometry with rFSE (500 32x32 losses over 8 images, F = 128,
+    100 basis functions): the interior blocks fused, the clipped ones per
+    window, every block gated against the C oracle."""
+    from paper_2204_14193_b200.synth import field
+    import torch
+    imgs = np.stack([field(512, 512, seed=40 + k) for k in range(8)]).astype(np.float32)
+    blocks = np.array([(f, 64 * i, 64 * j) for f in range(8) for i in range(8) for j in range(8)],
+                      np.int32)[:500]
+    plan = fse.ConcealPlan(blocks, 512, 512, fse.Geometry(32, 16, 128), rho_hat=0.8, gamma=0.5,
+                           algorithm="rfse", precision="fp32", iterations=100, basis_target=100)
+    assert plan.info["fast_path"] == 1
+    t32, tr = plan.run(torch.from_numpy(imgs).cuda(), tile_dtype="f32", trace=True)
+    print(_rfse_gate(fse, imgs, blocks, t32, tr, None, 128, 32, 100, 100, log="rfse128_config4b",
+                     border=16))
