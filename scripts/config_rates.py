@@ -34,6 +34,7 @@ def report(name, plan, frames, n, F, I, tile_dtype=None, reps=20, **extra):
          "smem_frac_nominal": rate * 8 * F * F * I / PEAK, "plan": plan.info}
     if I != 100:
         d["blocks_per_s_100it_equiv"] = rate * I / 100
+    if I != 100 or F != 64:  # configs with I != 100 or B != 16
         d["bin_iterations_per_s"] = rate * F * F * I
     d.update(extra)
     print(json.dumps(d), flush=True)
