@@ -412,7 +412,7 @@ static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int 
   // both axes (every unclipped window) has real centred weight spectra; the
   // fused cFSE kernel then iterates on one real table value per bin, and the
   // fused rFSE kernel at F = 128 exists only in that frame.
-  // FSE_SYM=0 keeps every cFSE class on the complex W' table.
+  // FSE_SYM=0 keeps every class on the complex W' table (except F = 128 rFSE).
   std::vector<int32_t> symc(std::max(nc, 1), 0);
   for (int c = 0; c < nc; ++c) {
     const int8_t *L = labels.data() + (size_t)c * F * F;
@@ -447,7 +447,7 @@ static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int 
 
   std::vector<int32_t> sym(std::max(nc, 1), 0);
   for (int c = 0; c < nc; ++c) {
-    sym[c] = p->fast && symc[c] && (rf128 || (algorithm == FSE_ALG_CFSE && sym_allowed));
+    sym[c] = p->fast && symc[c] && (rf128 || sym_allowed);
     p->n_sym += sym[c];
   }
   CK(p->alloc(&p->class_sym, (size_t)std::max(nc, 1)));

@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     }
     // centred frame: the class's weights are mirror-symmetric and its table
     // is the real Q (see the iteration section); uniform over the CTA
-    const bool sym = (ALG == 0 || F == 128) && a.class_sym && __ldg(a.class_sym + cls);
+    const bool sym = a.class_sym && __ldg(a.class_sym + cls);
     const int b = __ldg(a.rounds + (size_t)round * NS + slot);
     if (b < 0) {  // idle this round: keep the slot's prefetch chain going
       if constexpr (TMA) prefetch(round + gridDim.x);
@@ -1392,6 +1392,100 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           (unsigned)__cvta_generic_to_shared(region + G::TABLE_BYTES + F * F / 2 * sizeof(float4)) +
               (unsigned)(rowbase * 32 + lane) * 8u,
           lane);
+#ifndef FSE_RSYM
+#define FSE_RSYM 1  // centred-frame rFSE for mirror-symmetric classes at F = 32 / 64
+#endif
+      if (FSE_RSYM && sym) {
+        // Centred frame (interior classes), as the F = 128 rFSE loop: crit =
+        // alpha R~.re^2 + beta R~.im^2 with per-bin (alpha, beta) in the
+        // pair-criterion table's place (one float4 (alpha_a, alpha_b,
+        // beta_a, beta_b) per bin pair, doubled-frequency wraps already
+        // applied), the update reads the real Q pair table (one LDS.64 per
+        // atom) at both atoms' shifts, the mirror atom with sg conj(c~).
+        constexpr unsigned RSB = (F == 32 ? 2u : 1u) * (unsigned)G::SYM_C * 8u;  // bytes per pair step
+        const unsigned crit0 = (unsigned)__cvta_generic_to_shared(region + G::TABLE_BYTES);
+        unsigned midx = 0;
+        float c2re = 0.f, c2im = 0.f;
+        int tally = 0;
+        nit = 0;
+#pragma unroll 1
+        for (int it = 0; it < a.iterations && tally < a.stop_tally; ++it) {
+          const unsigned k0 = kpos + (unsigned)(G::SYM_C - F) * (kpos >> G::LOG) + (unsigned)((F - 1) * (G::SYM_C + 1));
+          const unsigned tq1 = tbase + ((k0 - gidx - (unsigned)(G::SYM_C - F) * (gidx >> G::LOG)) << 3);
+          const unsigned tq2 = tbase + ((k0 - midx - (unsigned)(G::SYM_C - F) * (midx >> G::LOG)) << 3);
+          float bst = -1.f, bxs = 0.f;
+          int bps = 0;
+#pragma unroll
+          for (int p = 0; p < G::NP; ++p) {
+            FSE_CHECK((tq1 - tbase) / 8 + (unsigned)p * (RSB / 8) < (unsigned)(G::SYM_R * G::SYM_C));
+            FSE_CHECK((tq2 - tbase) / 8 + (unsigned)p * (RSB / 8) < (unsigned)(G::SYM_R * G::SYM_C));
+            const float2 q1 = lds64f(tq1 + (unsigned)p * RSB), q2 = lds64f(tq2 + (unsigned)p * RSB);
+            ffma2_acc(Rre[p], q1, -cre);
+            ffma2_acc(Rim[p], q1, -cim);
+            ffma2_acc(Rre[p], q2, -c2re);
+            ffma2_acc(Rim[p], q2, -c2im);
+            const float4 ab = lds128f(rt4 + (unsigned)(p * 32 * 16));  // (alpha_a, alpha_b, beta_a, beta_b)
+            const float2 t1 = fmul2(make_float2(ab.x, ab.y), Rre[p]);
+            const float2 t2 = fmul2(make_float2(ab.z, ab.w), Rim[p]);
+            float2 cr = fmul2(t1, Rre[p]);
+            cr = ffma2(t2, Rim[p], cr);
+            first_max(bst, bps, bxs, cr, p);
+          }
+          const int myidx = bin_index<F>(w, lane, bps, bxs >= bst ? 0 : 1);
+          const unsigned key = __float_as_uint(fmaxf(bst, 0.f));  // monotone as unsigned
+          const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
+          const unsigned widx =
+              __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
+          int pw, mw, ow;
+          decode_bin<F>((int)widx, w, pw, mw, ow);
+          float are, aim;
+          pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
+          are = __shfl_sync(0xffffffffu, are, ow);
+          aim = __shfl_sync(0xffffffffu, aim, ow);
+          gidx = widx;
+          unsigned gkey = wmax;
+          if constexpr (G::NW == 2) {
+            if (lane == 0)
+              sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
+            slot_sync<F>(slot);
+            const uint4 o = lds128u(xc + 16u * (unsigned)(w ^ 1));
+            if (o.x > wmax || (o.x == wmax && o.y < widx)) {
+              gidx = o.y;
+              gkey = o.x;
+              are = __uint_as_float(o.z);
+              aim = __uint_as_float(o.w);
+            }
+            xc ^= (unsigned)(G::NW * sizeof(uint4));
+          }
+          // (alpha, beta) of the chosen bin: its table entry and member
+          const unsigned u = gidx >> G::LOG, v = gidx & (F - 1);
+          const bool self = ((2 * u) & (F - 1)) == 0 && ((2 * v) & (F - 1)) == 0;
+          const unsigned ent = F == 32 ? (u >> 1) * 32u + v : u * 32u + (v & 31u);
+          const bool mb = F == 32 ? (u & 1u) != 0u : ((v >> 5) & 1u) != 0u;
+          const float4 e4 = lds128f(crit0 + ent * 16u);
+          const float fac = self ? 1.f : 0.5f;
+          float pr = fac * (mb ? e4.y : e4.x) * are, pi = fac * (mb ? e4.w : e4.z) * aim;
+          const float sg = ((u != 0u) != (v != 0u)) ? -1.f : 1.f;
+          unsigned mi = (((F - u) & (F - 1)) << G::LOG) | ((F - v) & (F - 1));
+          if (!self && mi < gidx) {  // canonical member (rfse.py:113-121)
+            const unsigned t = gidx;
+            gidx = mi;
+            mi = t;
+            pr = sg * pr;
+            pi = -sg * pi;
+          }
+          midx = self ? gidx : mi;
+          cre = a.gamma * pr;
+          cim = a.gamma * pi;
+          c2re = self ? 0.f : sg * cre;
+          c2im = self ? 0.f : -sg * cim;
+          tally += self ? 1 : 2;
+          if (st == 0)
+            sp.trace[it] = make_float4(__uint_as_float(gidx | (self ? 0x80000000u : 0u)), cre, cim,
+                                       __uint_as_float(gkey));
+          nit = it + 1;
+        }
+      } else {
       unsigned midx = 0;            // bin of the previous pick's second atom
       float c2re = 0.f, c2im = 0.f;  // its coefficient (conj c, or 0 after a self-conjugate pick)
       int tally = 0;
@@ -1494,6 +1588,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           sp.trace[it] = make_float4(__uint_as_float(gidx | (self ? 0x80000000u : 0u)), cre, cim,
                                      __uint_as_float(gkey));
         nit = it + 1;
+      }
       }
     }
     slot_sync<F>(slot);
@@ -1863,6 +1958,38 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
     for (int i = threadIdx.x; i < R * C; i += blockDim.x) {
       const int r = i / C, cc = i - r * C, qi = r - (F - 1), qj = cc - (F - 1);
       E[i] = make_float2(q(qi, qj), q(qi + di, qj + dj));
+    }
+    if (a.rfse) {
+      // centred rFSE criterion (the kernel's centred rFSE loop): per bin
+      // pair of the thread layout (as the complex path's A4 entries)
+      // (alpha_a, alpha_b, beta_a, beta_b), alpha = 2 / (W00 + s Q0), beta =
+      // 2 / (W00 - s Q0) at the doubled frequency, s = -1 per doubled row or
+      // column that wraps past F; self-conjugate bins (1 / W00, 0), swapped
+      // when s = -1 (exactly the bins whose phase factor is imaginary)
+      const double w00 = W[0].x;
+      float4 *A4 = (float4 *)(tab + (F == 32 ? FG<32>::TABLE_BYTES : FG<64>::TABLE_BYTES));
+      for (int i = threadIdx.x; i < FF / 2; i += blockDim.x) {
+        const int r = i >> 5, cc = i & 31;
+        double al[2], be[2];
+        for (int h = 0; h < 2; ++h) {
+          const int br = F == 32 ? 2 * r + h : r, bc = F == 32 ? cc : cc + 32 * h;
+          const int r2 = 2 * br, c2 = 2 * bc;
+          const bool flip = (r2 >= F) != (c2 >= F);
+          const int k2 = r2 % F, l2 = c2 % F;
+          double x, y;
+          if (k2 == 0 && l2 == 0) {
+            x = 1.0 / w00;
+            y = 0.0;
+          } else {
+            const double q0 = T[k2 * F + l2].x;
+            x = 2.0 / (w00 + q0);
+            y = 2.0 / (w00 - q0);
+          }
+          al[h] = flip ? y : x;
+          be[h] = flip ? x : y;
+        }
+        A4[i] = make_float4((float)al[0], (float)al[1], (float)be[0], (float)be[1]);
+      }
     }
     return;
   }

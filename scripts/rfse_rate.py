@@ -13,8 +13,17 @@ nf = 32 if F == 64 else 8
 border = 16 if F == 128 else F // 4
 frames = field_torch(nf, 2160, 3840, seed=5, device="cuda", edges=True)
 blocks = fse.frames_pattern(nf, 2160, 3840, F // 4, 0.04 if F == 128 else 0.05, seed=5)
+# interior blocks only (every window unclipped: all fused; at F = 128 the
+# clipped rFSE windows otherwise run on the per-window kernel)
+off = (F - F // 4) // 2
+inner = blocks[(blocks[:, 1] >= off) & (blocks[:, 2] >= off) & (blocks[:, 1] + F - off <= 2160) &
+               (blocks[:, 2] + F - off <= 3840)]
 for bf in (100, 200):
-    for alg in ("cfse", "rfse"):
+    for alg in ("cfse", "rfse", "rfse-interior"):
+        blocks_all = blocks
+        if alg == "rfse-interior":
+            blocks, alg = inner, "rfse"
+        name = "rfse-interior" if blocks is inner else alg
         kw = dict(iterations=bf) if alg == "cfse" else dict(iterations=bf, basis_target=bf)
         plan = fse.ConcealPlan(blocks, 2160, 3840, fse.Geometry(F // 4, border, F), rho_hat=0.8, gamma=0.5,
                                algorithm=alg, **kw)
@@ -34,7 +43,8 @@ for bf in (100, 200):
         per_bin = 8 if alg == "cfse" else 28
         tbps = len(blocks) / s * its * F * F * per_bin / 1e12
         peak = torch.cuda.get_device_properties(0).multi_processor_count * 128 * 1965e6 / 1e12
-        print(json.dumps({"F": F, "algorithm": alg, "basis_functions": bf, "blocks": len(blocks),
+        print(json.dumps({"F": F, "algorithm": name, "basis_functions": bf, "blocks": len(blocks),
                           "blocks_per_s": len(blocks) / s, "us_per_block": s / len(blocks) * 1e6,
                           "mean_iterations": its, "smem_bytes_per_bin_iteration": per_bin,
                           "smem_TBps": tbps, "frac_nominal": tbps / peak, "plan": plan.info}))
+        blocks = blocks_all
