@@ -73,8 +73,14 @@ template <int F> struct FG {
   static constexpr bool PLANAR = F == 128;  // planar re/im table (pair table would not fit)
   // rows of the row-extended table: the thread walks rows rowoff + step*p
   static constexpr int TROWS = F == 32 ? F + 31 : F + RPW - 1;
-  static constexpr size_t TABLE_BYTES =
+  // class region: the complex W' table or the centred-frame Q table (below),
+  // whichever is larger
+  static constexpr size_t CPLX_BYTES =
       PLANAR ? (size_t)TROWS * F * 2 * sizeof(float) : (size_t)TROWS * F * sizeof(float4);
+  static constexpr size_t SYM_BYTES =
+      F == 128 ? (size_t)(2 * F - 1) * F * sizeof(float)
+               : (size_t)(F == 32 ? 62 : 2 * F - 1) * (F == 32 ? 63 : F + 31) * sizeof(float2);
+  static constexpr size_t TABLE_BYTES = ((CPLX_BYTES > SYM_BYTES ? CPLX_BYTES : SYM_BYTES) + 15) & ~(size_t)15;
   // real half-spectrum FFT scratch: max(F/2 x (F+1), F x (F/2+1)) complex
   static constexpr size_t SCRATCH = (((size_t)F * (F / 2 + 1) * sizeof(float2) + 15) & ~(size_t)15);
   static constexpr int B = F / 4;  // loss block edge (the planner's fast-path condition)
