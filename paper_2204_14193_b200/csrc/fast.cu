@@ -353,7 +353,17 @@ FSE_DEV void pick_bin(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p, i
 #define FSE_GROUPMAX32 FSE_GROUPMAX
 #endif
 #ifndef FSE_GROUPMAX64
+#ifdef FSE_GROUPMAX
 #define FSE_GROUPMAX64 FSE_GROUPMAX
+#else
+// F=64: groups of 2 bin pairs (measured with the centred-frame loop and a
+// W' prefetch depth of 4: 7.88 -> 8.21 M blocks/s on config 5, bitwise
+// identical tiles and traces; each knob alone: +0.8 % / +0.0 %)
+#define FSE_GROUPMAX64 2
+#endif
+#endif
+#ifndef FSE_PREFETCH64
+#define FSE_PREFETCH64 4  // F=64 table-load prefetch depth (with FSE_GROUPMAX64 = 2)
 #endif
 #ifndef FSE_GROUPMAX128
 #define FSE_GROUPMAX128 FSE_GROUPMAX
@@ -962,7 +972,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
 #ifndef FSE_PREFETCH
 #define FSE_PREFETCH 2
 #endif
-        constexpr int PD = FSE_PREFETCH;
+        constexpr int PD = F == 64 ? FSE_PREFETCH64 : FSE_PREFETCH;
         constexpr unsigned RSB = (F == 32 ? 2u : 1u) * (unsigned)G::SYM_C * 8u;  // bytes per pair step
         // entry of (row rowbase - u, column lane - v): with kpos = rowbase F + lane
         // and gidx = u F + v, (rowbase - u + F - 1) SYM_C + lane - v + F - 1 =
@@ -1019,7 +1029,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         // W' loads issued PD pairs ahead of their use (0: left to ptxas).  Without
         // it ptxas may keep only two load buffers in flight when registers are
         // tight, exposing the shared-memory latency (measured -10%).
-        constexpr int PD = FSE_PREFETCH;
+        constexpr int PD = F == 64 ? FSE_PREFETCH64 : FSE_PREFETCH;
         float4 wbuf[PD > 0 ? PD : 1];
 #pragma unroll
         for (int d = 0; d < PD; ++d) wbuf[d] = lds128f(tp + (unsigned)((F == 32 ? 2 * d : d) * F * 16));
