@@ -170,9 +170,8 @@ int fse_plan_create(fse_plan **plan, const int32_t *blocks, int n_blocks, int H,
  * iterations, rFSE stops each block once its basis-function tally (2 per
  * pair pick, 1 per self-conjugate pick) reaches it, with at most
  * basis_target iterations (types.py:55-60, rfse.py:184-189).  The fused fp32
- * kernel serves rFSE at F = 32 and 64, and at F = 128 for unclipped windows (the
- * plan's clipped F = 128 windows run the per-window kernel, their tiles and
- * traces scattered into place); other sizes and fp64 use the generic kernel.
+ * kernel serves rFSE at F = 32, 64 and 128; other sizes and fp64 use the generic
+ * kernel.
  * Errors additionally: FSE_ERR_CONFIG for a support degenerate for pairwise
  * selection (rfse.py:50-55). */
 int fse_plan_create_ex(fse_plan **plan, const int32_t *blocks, int n_blocks, int H, int W, int B,

@@ -40,6 +40,9 @@ def fp32_gate(frames, blocks, tiles_gpu, traces_gpu, F, B, border, rho, gamma, i
     ref = orc.conceal_blocks(fr, blocks, B, border, F, rho, gamma, iters)
     g = np.asarray(tiles_gpu, np.float64)
     dev = np.abs(g - ref).reshape(len(blocks), -1).max(axis=1)
+    # a non-finite tile is a failure, never an outlier to certify
+    nonfinite = [(int(k), "non-finite tile") for k in np.nonzero(~np.isfinite(dev))[0]]
+    assert not nonfinite, f"fp32 tiles with NaN/Inf: {nonfinite[:10]}"
     bad = np.nonzero(dev > px_tol)[0]
     outliers, failed = [], []
     for k in bad:
@@ -98,6 +101,8 @@ def rfse_gate(frames, blocks, tiles_gpu, traces_gpu, F, B, border, rho, gamma, i
     ref = orc.conceal_blocks_rfse(fr, blocks, B, border, F, rho, gamma, iters, basis_target)
     g = np.asarray(tiles_gpu, np.float64)
     dev = np.abs(g - ref).reshape(len(blocks), -1).max(axis=1)
+    nonfinite = [(int(k), "non-finite tile") for k in np.nonzero(~np.isfinite(dev))[0]]
+    assert not nonfinite, f"fp32 rFSE tiles with NaN/Inf: {nonfinite[:10]}"
     outliers, failed = [], []
     for k in np.nonzero(dev > px_tol)[0]:
         f, t, l = blocks[k]

@@ -121,16 +121,6 @@ struct fse_plan {
   int32_t *status = nullptr;
   int32_t *selfs = nullptr, *counts = nullptr, *tallies = nullptr;  // generic rFSE outputs
   void *gen_ws = nullptr;
-  // F = 128 rFSE plans with clipped classes: the fused kernel conceals the
-  // centred-frame (interior) blocks, this per-window child plan the rest;
-  // its tiles / traces land in staging buffers and are scattered to the
-  // blocks' positions (rest_idx: child block -> parent block)
-  struct fse_plan *rest = nullptr;
-  int n_rest = 0;
-  int32_t *rest_idx = nullptr;
-  char *rest_tiles = nullptr;
-  int32_t *rest_uv = nullptr;
-  float *rest_c = nullptr, *rest_e = nullptr;
   std::vector<void *> owned;
 
   template <typename T> cudaError_t alloc(T **p, size_t n) {
@@ -139,7 +129,6 @@ struct fse_plan {
     return e;
   }
   ~fse_plan() {
-    delete rest;
     for (void *p : owned) cudaFree(p);
   }
 };
@@ -293,22 +282,10 @@ int fse_plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, 
                             precision, FSE_ALG_CFSE, -1, stream);
 }
 
-static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, int W, int B,
-                       int border, int F, double rho, double gamma, int iterations, int precision,
-                       int algorithm, int basis_target, void *stream, bool force_generic);
-
 int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int H, int W, int B,
                        int border, int F, double rho, double gamma, int iterations, int precision,
                        int algorithm, int basis_target, void *stream) {
-  return plan_create(out, blocks, n_blocks, H, W, B, border, F, rho, gamma, iterations, precision,
-                     algorithm, basis_target, stream, false);
-}
-
-static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int H, int W, int B,
-                       int border, int F, double rho, double gamma, int iterations, int precision,
-                       int algorithm, int basis_target, void *stream, bool force_generic) {
   if (!out) return fail(FSE_ERR_VALUE, "null plan pointer");
-  const int iterations_arg = iterations;
   if (algorithm != FSE_ALG_CFSE && algorithm != FSE_ALG_RFSE)
     return fail(FSE_ERR_CONFIG, "algorithm must be cfse (0) or rfse (1), got %d", algorithm);
   // basis_target (types.py:55-60, rfse.py:184-189): cFSE runs that many
@@ -410,9 +387,9 @@ static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int 
 
   // Centred frame (fast.cu): a class whose label map is mirror-symmetric in
   // both axes (every unclipped window) has real centred weight spectra; the
-  // fused cFSE kernel then iterates on one real table value per bin, and the
-  // fused rFSE kernel at F = 128 exists only in that frame.
-  // FSE_SYM=0 keeps every class on the complex W' table (except F = 128 rFSE).
+  // fused kernels then iterate on one real table value per bin (cFSE) or
+  // per atom and bin (rFSE).  FSE_SYM=0 keeps every class on the complex W'
+  // table.
   std::vector<int32_t> symc(std::max(nc, 1), 0);
   for (int c = 0; c < nc; ++c) {
     const int8_t *L = labels.data() + (size_t)c * F * F;
@@ -424,21 +401,9 @@ static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int 
   }
   const char *sym_env = getenv("FSE_SYM");
   const bool sym_allowed = !(sym_env && atoi(sym_env) == 0);
-  p->fast = !force_generic && precision == FSE_PREC_F32 &&
+  p->fast = precision == FSE_PREC_F32 &&
             fse::fast_config(F, iterations, sm_count(), &p->cfg, algorithm) &&
             B * B == 2 * (F * F / 32) && iterations > 0;
-  const bool rf128 = algorithm == FSE_ALG_RFSE && F == 128;
-  std::vector<int32_t> rest_blocks;  // F = 128 rFSE: clipped-class blocks -> per-window child
-  if (p->fast && rf128) {
-    int ns = 0;
-    for (int c = 0; c < nc; ++c) ns += symc[c];
-    if (ns == 0) {
-      p->fast = false;
-    } else if (ns < nc) {
-      for (int b = 0; b < n_blocks; ++b)
-        if (!symc[bclass[b]]) rest_blocks.push_back(b);
-    }
-  }
   double *dmin_dev = nullptr;  // rfse.py:47-55 degeneracy check, every rFSE plan
   if (algorithm == FSE_ALG_RFSE) CK(p->alloc(&dmin_dev, (size_t)std::max(nc, 1)));
   if (p->fast) CK(p->alloc((char **)&p->table, (size_t)nc * p->cfg.table_bytes));
@@ -447,7 +412,7 @@ static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int 
 
   std::vector<int32_t> sym(std::max(nc, 1), 0);
   for (int c = 0; c < nc; ++c) {
-    sym[c] = p->fast && symc[c] && (rf128 || sym_allowed);
+    sym[c] = p->fast && symc[c] && sym_allowed;
     p->n_sym += sym[c];
   }
   CK(p->alloc(&p->class_sym, (size_t)std::max(nc, 1)));
@@ -486,8 +451,7 @@ static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int 
     // (config 2, 256 blocks: 165 -> 108 us; FSE_SPREAD=0 packs full rounds).
     const int Sl = p->cfg.slots;
     std::vector<std::vector<int32_t>> by(nc);
-    for (int b = 0; b < n_blocks; ++b)
-      if (!rf128 || symc[bclass[b]]) by[bclass[b]].push_back(b);
+    for (int b = 0; b < n_blocks; ++b) by[bclass[b]].push_back(b);
     int use = Sl;
     const char *spread_env = getenv("FSE_SPREAD");
     if (!spread_env || atoi(spread_env) != 0) {
@@ -532,26 +496,6 @@ static int plan_create(fse_plan **out, const int32_t *blocks, int n_blocks, int 
     }
     size_t ws = fse::generic_workspace_bytes((int)C, F, F, precision);
     if (ws) CK(p->alloc((char **)&p->gen_ws, ws));
-  }
-  if (!rest_blocks.empty()) {
-    const int nr = (int)rest_blocks.size();
-    std::vector<int32_t> rb((size_t)nr * 3);
-    for (int i = 0; i < nr; ++i)
-      for (int j = 0; j < 3; ++j) rb[3 * i + j] = blocks[3 * rest_blocks[i] + j];
-    fse_plan *child = nullptr;
-    if (int r = plan_create(&child, rb.data(), nr, H, W, B, border, F, rho, gamma, iterations_arg,
-                            precision, algorithm, basis_target, stream, true))
-      return r;
-    p->rest = child;
-    p->n_rest = nr;
-    const size_t It = (size_t)std::max(child->iterations, 1);
-    CK(p->alloc(&p->rest_idx, (size_t)nr));
-    CK(p->alloc(&p->rest_tiles, (size_t)nr * B * B * sizeof(double)));
-    CK(p->alloc(&p->rest_uv, (size_t)nr * It * 2));
-    CK(p->alloc(&p->rest_c, (size_t)nr * It * 2));
-    CK(p->alloc(&p->rest_e, (size_t)nr * It));
-    CK(cudaMemcpyAsync(p->rest_idx, rest_blocks.data(), (size_t)nr * sizeof(int32_t),
-                       cudaMemcpyHostToDevice, st));
   }
   CK(cudaStreamSynchronize(st));
   *out = p.release();
@@ -642,21 +586,6 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
         a.use_tma = 1;
     }
     CK(fse::launch_fast(a, p->cfg, a.use_tma ? &tmap : nullptr, st));
-    if (p->rest) {  // clipped classes of an F = 128 rFSE plan: per-window kernel + scatter
-      const size_t esz = tile_dtype == 0 ? 1 : tile_dtype == 1 ? 4 : 8;
-      const size_t It = (size_t)p->rest->iterations;
-      if (int r = fse_plan_run(p->rest, frames, dtype, pitch, frame_stride, n_frames, p->rest_tiles,
-                               tile_dtype, trace_uv ? p->rest_uv : nullptr,
-                               trace_uv ? p->rest_c : nullptr, trace_uv ? p->rest_e : nullptr, stream))
-        return r;
-      CK(fse::launch_scatter_rows(p->rest_tiles, tiles, p->rest_idx, p->n_rest,
-                                  (size_t)p->B * p->B * esz, st));
-      if (trace_uv) {
-        CK(fse::launch_scatter_rows(p->rest_uv, trace_uv, p->rest_idx, p->n_rest, It * 2 * 4, st));
-        CK(fse::launch_scatter_rows(p->rest_c, trace_c, p->rest_idx, p->n_rest, It * 2 * 4, st));
-        CK(fse::launch_scatter_rows(p->rest_e, trace_e, p->rest_idx, p->n_rest, It * 4, st));
-      }
-    }
     return FSE_OK;
   }
   if (trace_uv && (!trace_c || !trace_e)) return fail(FSE_ERR_VALUE, "partial trace buffers");

@@ -207,17 +207,16 @@ FSE_DEV float4 lds128f(unsigned addr) {
 // a = R_w[k]:  crit = A a.re^2 + C a.im^2 - D a.re a.im  (rfse.py:86-111).
 // F = 32: sixteen one-warp blocks per CTA (the rFSE loop state needs up to
 // 128 registers), tables for bins (2p, c), (2p + 1, c) of pair p, column c.
-// F = 128: one block per CTA in the centred frame only (mirror-symmetric
-// classes; rFSE plans send clipped classes to the per-window kernel).  Its
-// pair criterion there needs two real coefficients per bin, alpha and beta
-// (below), which depend on the doubled frequency only: a 64 x 32 x 2 table
-// (32 KB) that each block copies into its FFT scratch after the setup
-// (the Q table leaves no room for it in the class region).
+// F = 128: one block per CTA.  Its pair-criterion coefficients depend on the
+// doubled frequency only: per doubled row (64) and lane, the lane's two
+// doubled columns -- centred frame (alpha, beta), 32 KB; complex frame (A, C,
+// -D), 48 KB -- a table each block copies into the tail of its FFT scratch
+// after the setup (the W' / Q table fills the class region).
 template <int F> constexpr int rf_slots() { return F == 32 ? 16 : F == 64 ? 4 : 1; }
 // pair-criterion tables: F^2 / 2 bin pairs x (float4 + float2); F = 128 the
 // centred alpha | beta halves, 64 doubled rows x 32 lanes x float2 each
 template <int F> constexpr size_t rf_t2_bytes() {
-  return F == 128 ? (size_t)2 * 64 * 32 * sizeof(float2)
+  return F == 128 ? (size_t)64 * 32 * (sizeof(float4) + sizeof(float2))
                   : (size_t)F * F / 2 * (sizeof(float4) + sizeof(float2));
 }
 template <int F, int ALG> struct KS {  // per-algorithm launch shape
@@ -656,11 +655,10 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     const int cls = __ldg(a.round_class + round);
     if (cls != loaded) {
       __syncthreads();
-      // (rFSE at F = 128: the Q table only; the criterion table goes to the
-      // scratch per block)
+      // (rFSE at F = 128: the W' / Q table only; the criterion table goes to
+      // the scratch per block)
       copy_table(region, (const char *)a.table + (size_t)cls * a.table_bytes,
-                 ALG && F == 128 ? (size_t)G::SYM_R * F * sizeof(float) : a.table_bytes, tid,
-                 blockDim.x);
+                 ALG && F == 128 ? G::TABLE_BYTES : a.table_bytes, tid, blockDim.x);
       __syncthreads();
       loaded = cls;
     }
@@ -1272,17 +1270,19 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       const unsigned crit_base = smem_u32(sp.scratch) + (unsigned)(G::SCRATCH - rf_t2_bytes<F>());
       {
         const char *src = (const char *)a.table + (size_t)cls * a.table_bytes + G::TABLE_BYTES;
-        for (int i = st; i < (int)(rf_t2_bytes<F>() / 16); i += G::NT)
+        const int n16 = (int)((sym ? 64 * 32 * 2 * sizeof(float2) : rf_t2_bytes<F>()) / 16);
+        for (int i = st; i < n16; i += G::NT)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(crit_base + 16u * (unsigned)i),
                        "l"(src + 16 * (size_t)i)
                        : "memory");
         asm volatile("cp.async.wait_all;" ::: "memory");
         slot_sync<F>(slot);
       }
-      constexpr unsigned HALF = (unsigned)(rf_t2_bytes<F>() / 2);  // alpha half | beta half
+      constexpr unsigned HALF = 64u * 32u * (unsigned)sizeof(float2);  // alpha half | beta half
       // this warp's entries: doubled row of row r = rowbase + rr is (r mod 64)
       // (rows >= 64 wrap: alpha <-> beta); pair p = 2 rr + q, q = 1 for the
       // lane's columns + 64 (their doubled columns wrap: swap again)
+      if (sym) {
       const unsigned cw = __shfl_sync(0xffffffffu, crit_base + (unsigned)((((rowbase & 63) * 32) + lane) * 8), lane);
       const unsigned pA = w >= 4 ? cw + HALF : cw, pB = w >= 4 ? cw : cw + HALF;
       const float *Tq = (const float *)region;
@@ -1389,6 +1389,124 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
                                      __uint_as_float(gkey));
         }
         nit = it + 1;
+      }
+      } else {
+        // Complex frame (clipped classes): the reference's quadratic form
+        // crit = A a.re^2 + C a.im^2 - D a.re a.im (rfse.py:93-103) with
+        // (A, C, -D) at the doubled frequency -- in this frame W[2k] needs no
+        // sign, and the lane's four columns share the two doubled columns
+        // (2 lane, 2 lane + 64) -- from the 48 KB scratch table (float4 (A_c1,
+        // A_c2, C_c1, C_c2) half, float2 (-D_c1, -D_c2) half); the update reads
+        // the planar W' table at both atoms' shifts (rows row-extended, columns
+        // mod F), the mirror atom with conj(c); the winner's projection uses
+        // W[2u, 2v] and the reference's divisions (fast path).
+        const unsigned cw4 = __shfl_sync(0xffffffffu, crit_base + (unsigned)((((rowbase & 63) * 32) + lane) * 16), lane);
+        const unsigned cw2 = cw4 + 64u * 32u * 16u - (unsigned)((((rowbase & 63) * 32) + lane) * 8);
+        const float *Tre = (const float *)region;
+        const float *Tim = Tre + G::TROWS * F;
+        const float w00 = 1.f / __ldg(a.inv_w00 + cls);
+        unsigned midx = 0;
+        float c2re = 0.f, c2im = 0.f;
+        int tally = 0;
+        nit = 0;
+#pragma unroll 1
+        for (int it = 0; it < a.iterations && tally < a.stop_tally; ++it) {
+          int co1[4], co2[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            co1[h] = (lane + 32 * h - (int)(gidx & (F - 1))) & (F - 1);
+            co2[h] = (lane + 32 * h - (int)(midx & (F - 1))) & (F - 1);
+          }
+          const int ro1 = (rowbase - (int)(gidx >> G::LOG)) & (F - 1);
+          const int ro2 = (rowbase - (int)(midx >> G::LOG)) & (F - 1);
+          float bst = -1.f, bxs = 0.f;
+          int bps = 0;
+          float4 e4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          float2 e2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int p = 0; p < G::NP; ++p) {
+            const int q = 2 * (p & 1), rr = p >> 1;
+            const int r1 = (ro1 + rr) * F, r2 = (ro2 + rr) * F;
+            FSE_CHECK(ro1 + rr < G::TROWS && ro2 + rr < G::TROWS);
+            const float2 wr = make_float2(Tre[r1 + co1[q]], Tre[r1 + co1[q + 1]]);
+            const float2 wi = make_float2(Tim[r1 + co1[q]], Tim[r1 + co1[q + 1]]);
+            const float2 qr = make_float2(Tre[r2 + co2[q]], Tre[r2 + co2[q + 1]]);
+            const float2 qi = make_float2(Tim[r2 + co2[q]], Tim[r2 + co2[q + 1]]);
+            ffma2_acc(Rre[p], wr, -cre);
+            ffma2_acc(Rre[p], wi, cim);
+            ffma2_acc(Rim[p], wi, -cre);
+            ffma2_acc(Rim[p], wr, -cim);
+            ffma2_acc(Rre[p], qr, -c2re);
+            ffma2_acc(Rre[p], qi, c2im);
+            ffma2_acc(Rim[p], qi, -c2re);
+            ffma2_acc(Rim[p], qr, -c2im);
+            if (q == 0) {
+              e4 = lds128f(cw4 + (unsigned)(rr * 32 * 16));
+              e2 = lds64f(cw2 + (unsigned)(rr * 32 * 8));
+            }
+            float2 t1 = fmul2(make_float2(e4.x, e4.y), Rre[p]);
+            t1 = ffma2(e2, Rim[p], t1);
+            const float2 t2 = fmul2(make_float2(e4.z, e4.w), Rim[p]);
+            float2 cr = fmul2(t1, Rre[p]);
+            cr = ffma2(t2, Rim[p], cr);
+            first_max(bst, bps, bxs, cr, p);
+          }
+          const int myidx = bin_index<F>(w, lane, bps, bxs >= bst ? 0 : 1);
+          const unsigned key = __float_as_uint(fmaxf(bst, 0.f));  // monotone as unsigned
+          const unsigned wmax = __reduce_max_sync(0xffffffffu, key);
+          const unsigned widx = __reduce_min_sync(0xffffffffu, key == wmax ? (unsigned)myidx : 0xffffffffu);
+          int pw, mw, ow;
+          decode_bin<F>((int)widx, w, pw, mw, ow);
+          float are, aim;
+          pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
+          are = __shfl_sync(0xffffffffu, are, ow);
+          aim = __shfl_sync(0xffffffffu, aim, ow);
+          if (lane == 0) sts128u(xc + 16u * w, make_uint4(wmax, widx, __float_as_uint(are), __float_as_uint(aim)));
+          slot_sync<F>(slot);
+          const uint4 cnd = lane < G::NW ? lds128u(xc + 16u * lane) : make_uint4(0u, 0xffffffffu, 0u, 0u);
+          const unsigned gkey = __reduce_max_sync(0xffffffffu, cnd.x);
+          gidx = __reduce_min_sync(0xffffffffu, cnd.x == gkey ? cnd.y : 0xffffffffu);
+          const int wl = (int)(gidx / (unsigned)(G::RPW * F));
+          are = __shfl_sync(0xffffffffu, __uint_as_float(cnd.z), wl);
+          aim = __shfl_sync(0xffffffffu, __uint_as_float(cnd.w), wl);
+          xc ^= (unsigned)(G::NW * sizeof(uint4));
+          // joint projection of the chosen bin (rfse.py:93-103)
+          const unsigned u = gidx >> G::LOG, v = gidx & (F - 1);
+          const bool self = ((2 * u) & (F - 1)) == 0 && ((2 * v) & (F - 1)) == 0;
+          float pr, pi;
+          if (self) {
+            pr = __fdividef(are, w00);
+            pi = 0.f;
+          } else {
+            const int wi2 = (int)((((2 * u) & (F - 1)) * F) + ((2 * v) & (F - 1)));
+            const float wx = Tre[wi2], wy = Tim[wi2];
+            const float nr = w00 * are - (wx * are + wy * aim);
+            const float ni = w00 * aim - (wy * are - wx * aim);
+            const float d = w00 * w00 - (wx * wx + wy * wy);
+            const float rd = __fdividef(1.f, d);
+            pr = nr * rd;
+            pi = ni * rd;
+          }
+          unsigned mi = (((F - u) & (F - 1)) << G::LOG) | ((F - v) & (F - 1));
+          if (!self && mi < gidx) {  // canonical member (rfse.py:113-121)
+            const unsigned t = gidx;
+            gidx = mi;
+            mi = t;
+            pi = -pi;
+          }
+          midx = self ? gidx : mi;
+          cre = a.gamma * pr;
+          cim = a.gamma * pi;
+          c2re = self ? 0.f : cre;
+          c2im = self ? 0.f : -cim;
+          tally += self ? 1 : 2;
+          if (st == 0) {
+            FSE_CHECK(a.trace_scratch || (unsigned)it * 16u < (unsigned)(G::SCRATCH - rf_t2_bytes<F>()));
+            sp.trace[it] = make_float4(__uint_as_float(gidx | (self ? 0x80000000u : 0u)), cre, cim,
+                                       __uint_as_float(gkey));
+          }
+          nit = it + 1;
+        }
       }
     } else {
       // ---------------------------------------- rFSE (rfse.py:69-160)
@@ -1782,9 +1900,12 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algor
   int S;
   if (algorithm == 1) {  // fused rFSE: F = 32, 64; F = 128 centred-frame classes only
     if (F != 32 && F != 64 && F != 128) return false;
-    cfg->global_trace = iterations > (F == 32   ? FG<32>::TRACE_CAP
-                                      : F == 64 ? FG<64>::TRACE_CAP
-                                                : FG<128>::TRACE_CAP);
+    // (F = 128: the trace must also stay clear of the criterion table in the
+    // scratch tail during the iterations)
+    constexpr int cap128 = (int)((FG<128>::SCRATCH - rf_t2_bytes<128>()) / 16) < FG<128>::TRACE_CAP
+                               ? (int)((FG<128>::SCRATCH - rf_t2_bytes<128>()) / 16)
+                               : FG<128>::TRACE_CAP;
+    cfg->global_trace = iterations > (F == 32 ? FG<32>::TRACE_CAP : F == 64 ? FG<64>::TRACE_CAP : cap128);
     smem = F == 32 ? fast_smem<32, 1>(0) : F == 64 ? fast_smem<64, 1>(0) : fast_smem<128, 1>(0);
     if (smem > 227 * 1024) return false;
     cfg->slots = F == 32 ? rf_slots<32>() : F == 64 ? rf_slots<64>() : rf_slots<128>();
@@ -2017,6 +2138,34 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
       double2 x = W[(r % F) * F + q];
       Tre[i] = (float)x.x;
       Tim[i] = (float)x.y;
+    }
+    if (a.rfse) {
+      // complex-frame rFSE criterion at the doubled frequency (2 r2, 2 lane +
+      // 64 h): A = 2 (W00 - W2.re) / Dt, C = 2 (W00 + W2.re) / Dt, D = 4 W2.im /
+      // Dt, Dt = W00^2 - |W2|^2; (1 / W00, 0, 0) at (0, 0) (rfse.py:86-111)
+      const double w00 = W[0].x;
+      float4 *C4 = (float4 *)(tab + FG<128>::TABLE_BYTES);
+      float2 *C2 = (float2 *)(tab + FG<128>::TABLE_BYTES + 64 * 32 * sizeof(float4));
+      for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {
+        const int r2 = i >> 5, ln = i & 31;
+        double qa[2], qc[2], qd[2];
+        for (int h = 0; h < 2; ++h) {
+          const int k2 = 2 * r2, l2 = 2 * ln + 64 * h;
+          if (k2 == 0 && l2 == 0) {
+            qa[h] = 1.0 / w00;
+            qc[h] = 0.0;
+            qd[h] = 0.0;
+          } else {
+            const double2 w2 = W[k2 * F + l2];
+            const double d = w00 * w00 - (w2.x * w2.x + w2.y * w2.y);
+            qa[h] = 2.0 * (w00 - w2.x) / d;
+            qc[h] = 2.0 * (w00 + w2.x) / d;
+            qd[h] = 4.0 * w2.y / d;
+          }
+        }
+        C4[i] = make_float4((float)qa[0], (float)qa[1], (float)qc[0], (float)qc[1]);
+        C2[i] = make_float2((float)-qd[0], (float)-qd[1]);
+      }
     }
   } else {
     const int TR = F == 32 ? FG<32>::TROWS : FG<64>::TROWS;

@@ -1182,19 +1182,4 @@ cudaError_t launch_pack_trace(const int64_t *us, const int64_t *vs, const double
   return cudaGetLastError();
 }
 
-__global__ void scatter_rows_kernel(const uint32_t *src, uint32_t *dst, const int32_t *idx,
-                                    size_t row_words) {
-  const uint32_t *r = src + (size_t)blockIdx.x * row_words;
-  uint32_t *d = dst + (size_t)idx[blockIdx.x] * row_words;
-  for (size_t j = threadIdx.x; j < row_words; j += blockDim.x) d[j] = r[j];
-}
-
-cudaError_t launch_scatter_rows(const void *src, void *dst, const int32_t *idx, int n, size_t row_bytes,
-                                cudaStream_t s) {
-  if (n <= 0 || row_bytes == 0) return cudaSuccess;
-  if (row_bytes % 4) return cudaErrorInvalidValue;
-  scatter_rows_kernel<<<n, 128, 0, s>>>((const uint32_t *)src, (uint32_t *)dst, idx, row_bytes / 4);
-  return cudaGetLastError();
-}
-
 }  // namespace fse

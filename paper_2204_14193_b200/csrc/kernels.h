@@ -41,10 +41,6 @@ struct GenArgs {
 // windows (0 when everything fits in shared memory).
 size_t generic_workspace_bytes(int count, int M, int N, int precision);
 cudaError_t launch_generic_extrapolate(const GenArgs &a, void *workspace, cudaStream_t s);
-// dst row idx[i] = src row i (n rows of row_bytes, a multiple of 4): the
-// per-window child of a split plan writes into staging rows
-cudaError_t launch_scatter_rows(const void *src, void *dst, const int32_t *idx, int n, size_t row_bytes,
-                                cudaStream_t s);
 
 cudaError_t launch_cfse_kernel_f64(int count, int M, int N, double *R, const double *W,
                                    long long w_stride, double gamma, const double *inv_w00,

@@ -55,9 +55,8 @@ class ConcealPlan:
     blocks: int array (n, 3) = (frame, top, left) or (n, 2) = (top, left)
     for a single frame.  precision "fp32" uses the fused register-resident
     kernel (F in {32, 64, 128}); "fp64" the reference-exact per-window path.
-    algorithm "rfse" runs the conjugate-pair variant (rfse.py; fused in fp32 at
-    F=32, 64 and, for unclipped windows, F=128 -- clipped F=128 windows and
-    fp64 run per window); basis_target as in FseConfig.
+    algorithm "rfse" runs the conjugate-pair variant (rfse.py; fused in fp32,
+    per window in fp64); basis_target as in FseConfig.
     """
 
     def __init__(self, blocks, H: int, W: int, geometry: Geometry = Geometry(), *,

@@ -107,3 +107,23 @@ def test_rfse_certificate_of_a_forced_second_best_pick():
     cs2 = tr[2].copy()
     cs2[k - 1] *= 1 + 1e-3
     assert orc.rfse_divergence_certificate(s, lab, rho, gamma, k, (tr[0], tr[1], cs2))["err_amp"] > 0
+
+
+def test_gates_reject_non_finite_tiles():
+    """A NaN tile must fail the gate (|NaN - x| > tol is False, so it would
+    otherwise slip past the per-block check)."""
+    import numpy as np
+    import pytest
+    from oracle import oracle as orc
+    from oracle.gate import fp32_gate, rfse_gate
+    from paper_2204_14193_b200.synth import frame_u8
+    fr = frame_u8(96, 96, seed=2)
+    blocks = np.array([[0, 40, 40]], np.int32)
+    t = orc.conceal_blocks(fr, blocks, 16, 16, 64, 0.8, 0.5, 5)
+    t[0, 3, 3] = np.nan
+    with pytest.raises(AssertionError, match="NaN"):
+        fp32_gate(fr, blocks, t, None, 64, 16, 16, 0.8, 0.5, 5)
+    tr = orc.conceal_blocks_rfse(fr, blocks, 16, 16, 64, 0.8, 0.5, 5)
+    tr[0, 0, 0] = np.inf
+    with pytest.raises(AssertionError, match="NaN"):
+        rfse_gate(fr, blocks, tr, None, 64, 16, 16, 0.8, 0.5, 5)

@@ -357,14 +357,16 @@ def test_fused_rfse_on_a_config_frame(fse, F):
 # ---------------------------------------------------------------- F = 128
 
 
-@pytest.mark.parametrize("dtype,iters,bt", [("u8", 60, None), ("f32", 100, 100)])
-def test_fused_rfse128_split_plan(fse, dtype, iters, bt):
-    """F = 128 rFSE: interior blocks run the fused centred-frame kernel, the
-    clipped corner/edge blocks the per-window kernel (split plan, tiles and
-    traces scattered back to their positions).  Gate against the C oracle's
-    rFSE: every block within 0.5 gray levels except certified near-ties;
-    canonical members and the tally rule."""
+@pytest.mark.parametrize("dtype,iters,bt,sym", [("u8", 60, None, "1"), ("f32", 100, 100, "1"),
+                                                ("u8", 60, None, "0")])
+def test_fused_rfse128_mixed_classes(fse, dtype, iters, bt, sym, monkeypatch):
+    """F = 128 rFSE in one fused plan: interior blocks in the centred frame,
+    clipped corner/edge blocks on the complex W' table and (A, C, D)
+    criterion (FSE_SYM=0: every block on the complex path).  Gate against
+    the C oracle's rFSE: every block within 0.5 gray levels except certified
+    near-ties; canonical members and the tally rule."""
     import torch
+    monkeypatch.setenv("FSE_SYM", sym)
     from paper_2204_14193_b200.synth import field_torch
     H, W = 384, 544
     frames = field_torch(2, H, W, seed=29, device="cuda", edges=True)
@@ -376,10 +378,10 @@ def test_fused_rfse128_split_plan(fse, dtype, iters, bt):
     kw = dict(iterations=iters) if bt is None else dict(iterations=iters, basis_target=bt)
     plan = fse.ConcealPlan(blocks, H, W, fse.Geometry(32, 16, 128), rho_hat=0.8, gamma=0.5,
                            algorithm="rfse", precision="fp32", **kw)
-    assert plan.info["fast_path"] == 1 and plan.info["n_centred"] == 1
+    assert plan.info["fast_path"] == 1 and plan.info["n_centred"] == (1 if sym == "1" else 0)
     t32, tr = plan.run(frames, tile_dtype="f32", trace=True)
     print(_rfse_gate(fse, frames, blocks, t32, tr, None, 128, 32, iters, bt,
-                     log=f"rfse128_{dtype}_{iters}_{bt}", border=16))
+                     log=f"rfse128_{dtype}_{iters}_{bt}_sym{sym}", border=16))
     uv = tr["uv"].cpu().numpy()
     for k in range(len(blocks)):
         used = uv[k, :, 0] >= 0
@@ -426,8 +428,9 @@ def test_fused_rfse128_selection_sequence(fse):
 
 def test_fused_rfse128_config4b(fse):
     """Config 4b geometry with rFSE (500 32x32 losses over 8 images, F = 128,
-    100 basis functions): the interior blocks fused, the clipped ones per
-    window, every block gated against the C oracle."""
+    100 basis functions): interior blocks in the centred frame, the 115
+    clipped ones on the complex tables, every block gated against the C
+    oracle."""
     from paper_2204_14193_b200.synth import field
     import torch
     imgs = np.stack([field(512, 512, seed=40 + k) for k in range(8)]).astype(np.float32)
