@@ -355,14 +355,15 @@ FSE_DEV void pick_bin(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p, i
 #ifdef FSE_GROUPMAX
 #define FSE_GROUPMAX64 FSE_GROUPMAX
 #else
-// F=64: groups of 2 bin pairs (measured with the centred-frame loop and a
-// W' prefetch depth of 4: 7.88 -> 8.21 M blocks/s on config 5, bitwise
-// identical tiles and traces; each knob alone: +0.8 % / +0.0 %)
+// F=64: groups of 2 bin pairs (with the centred-frame loop: 7.88 -> 8.21 M
+// blocks/s on config 5 at a table prefetch depth of 4; with the FMNMX3 group
+// step (FSE_GMAX3) the best depth is 2 again: 8.36 M; bitwise identical tiles
+// and traces throughout)
 #define FSE_GROUPMAX64 2
 #endif
 #endif
 #ifndef FSE_PREFETCH64
-#define FSE_PREFETCH64 4  // F=64 table-load prefetch depth (with FSE_GROUPMAX64 = 2)
+#define FSE_PREFETCH64 2  // F=64 table-load prefetch depth (4 before the FMNMX3 group step)
 #endif
 #ifndef FSE_GROUPMAX128
 #define FSE_GROUPMAX128 FSE_GROUPMAX
@@ -397,6 +398,25 @@ template <int GM> FSE_DEV float group_max(const float (&v)[2 * GM]) {
 #pragma unroll
     for (int i = 1; i < 2 * GM; ++i) t = fmaxf(t, v[i]);
     return t;
+  }
+}
+
+#ifndef FSE_GMAX3
+// 1: the running maximum takes the group's last value in its FMNMX3 (one op on
+// the loop-carried chain, one ALU op fewer per group); 0: group maximum, then
+// compare and select against the running maximum.  Same result either way.
+#define FSE_GMAX3 1  // F=64 config 5: 8.15 -> 8.36 M blocks/s (bitwise identical)
+#endif
+// first-max step over a completed group g: bst = max(bst, group), bg = g when
+// the group holds a value strictly above the previous maximum
+template <int GM> FSE_DEV void group_step(const float (&v)[2 * GM], float &bst, int &bg, int g) {
+  if constexpr (FSE_GMAX3 && GM == 2) {
+    const float nb = fmax3(fmax3(v[0], v[1], v[2]), v[3], bst);
+    if (nb > bst) bg = g;
+    bst = nb;
+  } else {
+    const float t = group_max<GM>(v);
+    if (t > bst) { bst = t; bg = g; }
   }
 }
 
@@ -1007,10 +1027,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           } else if constexpr (GM > 0) {
             gv[2 * (p % GM)] = mg.x;
             gv[2 * (p % GM) + 1] = mg.y;
-            if (p % GM == GM - 1) {
-              const float t = group_max<GM>(gv);
-              if (t > bst[0]) { bst[0] = t; bg = p / GM; }
-            }
+            if (p % GM == GM - 1) group_step<GM>(gv, bst[0], bg, p / GM);
           } else {
             first_max(bst[ch], bps[ch], bxs[ch], mg, p);
           }
@@ -1061,10 +1078,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           } else if constexpr (GM > 0) {
             gv[2 * (p % GM)] = mg.x;
             gv[2 * (p % GM) + 1] = mg.y;
-            if (p % GM == GM - 1) {
-              const float t = group_max<GM>(gv);
-              if (t > bst[0]) { bst[0] = t; bg = p / GM; }
-            }
+            if (p % GM == GM - 1) group_step<GM>(gv, bst[0], bg, p / GM);
           } else {
             first_max(bst[ch], bps[ch], bxs[ch], mg, p);
           }
@@ -1100,10 +1114,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           if constexpr (GM > 0) {
             gv[2 * (p % GM)] = mg.x;
             gv[2 * (p % GM) + 1] = mg.y;
-            if (p % GM == GM - 1) {
-              const float t = group_max<GM>(gv);
-              if (t > bst[0]) { bst[0] = t; bg = p / GM; }
-            }
+            if (p % GM == GM - 1) group_step<GM>(gv, bst[0], bg, p / GM);
           } else {
             first_max(bst[ch], bps[ch], bxs[ch], mg, p);
           }
@@ -1131,10 +1142,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           if constexpr (GM > 0) {
             gv[2 * (p % GM)] = mg.x;
             gv[2 * (p % GM) + 1] = mg.y;
-            if (p % GM == GM - 1) {
-              const float t = group_max<GM>(gv);
-              if (t > bst[0]) { bst[0] = t; bg = p / GM; }
-            }
+            if (p % GM == GM - 1) group_step<GM>(gv, bst[0], bg, p / GM);
           } else {
             first_max(bst[ch], bps[ch], bxs[ch], mg, p);
           }
