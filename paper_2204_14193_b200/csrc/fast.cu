@@ -414,6 +414,10 @@ template <int GM> FSE_DEV void group_step(const float (&v)[2 * GM], float &bst, 
     const float nb = fmax3(fmax3(v[0], v[1], v[2]), v[3], bst);
     if (nb > bst) bg = g;
     bst = nb;
+  } else if constexpr (FSE_GMAX3 && GM == 4) {
+    const float nb = fmax3(fmax3(v[0], v[1], v[2]), fmax3(v[3], v[4], v[5]), fmax3(v[6], v[7], bst));
+    if (nb > bst) bg = g;
+    bst = nb;
   } else {
     const float t = group_max<GM>(v);
     if (t > bst) { bst = t; bg = g; }
@@ -1100,12 +1104,28 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         const float2 cr2[2] = {make_float2(-cre * sg[0], -cre * sg[1]), make_float2(-cre * sg[2], -cre * sg[3])};
         const float2 ci2[2] = {make_float2(-cim * sg[0], -cim * sg[1]), make_float2(-cim * sg[2], -cim * sg[3])};
         const int rq = rowbase - (int)(gidx >> G::LOG) + F - 1;
+#ifndef FSE_PREFETCH128
+#define FSE_PREFETCH128 0  // explicit table-load prefetch depth (0: left to ptxas)
+#endif
+        constexpr int PQ = FSE_PREFETCH128;
+        auto ldq = [&](int pp) {
+          const int r = (rq + (pp >> 1)) * F, q = pp & 1;
+          FSE_CHECK(rq + (pp >> 1) < G::SYM_R);
+          return make_float2(Tq[r + co[2 * q]], Tq[r + co[2 * q + 1]]);
+        };
+        float2 qb[PQ > 0 ? PQ : 1];
+#pragma unroll
+        for (int d = 0; d < PQ; ++d) qb[d] = ldq(d);
 #pragma unroll
         for (int p = 0; p < G::NP; ++p) {
-          const int r = (rq + (p >> 1)) * F;
           const int q = p & 1;
-          FSE_CHECK(rq + (p >> 1) < G::SYM_R);
-          const float2 qv = make_float2(Tq[r + co[2 * q]], Tq[r + co[2 * q + 1]]);
+          float2 qv;
+          if constexpr (PQ > 0) {
+            qv = qb[p % PQ];
+            if (p + PQ < G::NP) qb[p % PQ] = ldq(p + PQ);
+          } else {
+            qv = ldq(p);
+          }
           ffma2_acc2(Rre[p], qv, cr2[q]);
           ffma2_acc2(Rim[p], qv, ci2[q]);
           float2 mg = fmul2(Rre[p], Rre[p]);
