@@ -442,3 +442,34 @@ def test_fused_rfse128_config4b(fse):
     t32, tr = plan.run(torch.from_numpy(imgs).cuda(), tile_dtype="f32", trace=True)
     print(_rfse_gate(fse, imgs, blocks, t32, tr, None, 128, 32, 100, 100, log="rfse128_config4b",
                      border=16))
+
+
+@pytest.mark.parametrize("seed", range(_SEEDS or 4))
+def test_fused_rfse128_random_geometry(fse, seed):
+    """F = 128 fused rFSE on random image sizes (clipped windows on both
+    table kinds), positions, frame types and budgets, gated against the C
+    oracle (and the fp64 rFSE plan against the oracle at 1e-9)."""
+    import torch
+    from paper_2204_14193_b200.synth import field
+    rng = np.random.default_rng(7000 + seed)
+    H, W = int(rng.integers(40, 300)), int(rng.integers(40, 300))
+    n = int(rng.integers(4, 10))
+    blocks = np.stack([np.zeros(n, np.int64), rng.integers(0, H - 32 + 1, n),
+                       rng.integers(0, W - 32 + 1, n)], 1).astype(np.int32)
+    img = field(H, W, seed=seed)
+    dtype = rng.choice(["u8", "f32"])
+    img = np.clip(np.rint(img), 0, 255).astype(np.uint8) if dtype == "u8" else img.astype(np.float32)
+    iters = int(rng.choice([5, 30, 60]))
+    bt = None if rng.random() < 0.5 else int(rng.integers(1, 2 * iters + 1))
+    kw = dict(iterations=iters) if bt is None else dict(iterations=iters, basis_target=bt)
+    geo = fse.Geometry(32, 16, 128)
+    try:
+        fast = fse.ConcealPlan(blocks, H, W, geo, rho_hat=0.8, gamma=0.5, algorithm="rfse",
+                               precision="fp32", **kw)
+    except fse.ConfigError:
+        pytest.skip("degenerate pair geometry for this random image")
+    assert fast.info["fast_path"] == 1
+    fr = torch.from_numpy(np.ascontiguousarray(img)).cuda()
+    t32, tr32 = fast.run(fr, tile_dtype="f32", trace=True)
+    cert = _rfse_gate(fse, img, blocks, t32, tr32, None, 128, 32, iters, bt, border=16)
+    print(seed, H, W, dtype, iters, bt, "certified near-ties:", cert)
