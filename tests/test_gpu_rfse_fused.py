@@ -473,3 +473,22 @@ def test_fused_rfse128_random_geometry(fse, seed):
     t32, tr32 = fast.run(fr, tile_dtype="f32", trace=True)
     cert = _rfse_gate(fse, img, blocks, t32, tr32, None, 128, 32, iters, bt, border=16)
     print(seed, H, W, dtype, iters, bt, "certified near-ties:", cert)
+
+
+@pytest.mark.parametrize("F,B", [(64, 16), (32, 8)])
+def test_fused_rfse_complex_tables_on_interior_blocks(fse, F, B, monkeypatch):
+    """FSE_SYM=0 keeps interior classes on the complex W' / (A, C, D) tables
+    (the path of clipped classes): the same oracle gate as the centred
+    default, on a frame of interior and corner blocks."""
+    import torch
+    from paper_2204_14193_b200.synth import field_torch
+    monkeypatch.setenv("FSE_SYM", "0")
+    H, W = 240, 352
+    frames = field_torch(1, H, W, seed=31, device="cuda", edges=True)
+    blocks = fse.frames_pattern(1, H, W, B, 0.06, seed=9)
+    blocks = np.concatenate([blocks, np.array([[0, 0, 0], [0, H - B, W - B]], np.int32)])
+    plan = fse.ConcealPlan(blocks, H, W, fse.Geometry(B, B, F), rho_hat=0.8, gamma=0.5,
+                           algorithm="rfse", precision="fp32", iterations=60)
+    assert plan.info["fast_path"] == 1 and plan.info["n_centred"] == 0
+    t32, tr = plan.run(frames, tile_dtype="f32", trace=True)
+    print(_rfse_gate(fse, frames, blocks, t32, tr, None, F, B, 60, None, log=f"rfse{F}_complex"))
