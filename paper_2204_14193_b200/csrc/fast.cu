@@ -362,6 +362,13 @@ FSE_DEV void pick_bin(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int p, i
 #define FSE_GROUPMAX64 2
 #endif
 #endif
+#ifndef FSE_RTWIST
+// F=64 centred rFSE: "twisted" register pairs A = (re_a, im_b), B = (im_a, re_b)
+// so the pair criterion alpha re^2 + beta im^2 (member b: alpha and beta
+// swapped, its doubled column wraps) is alpha A^2 + beta B^2 with scalar
+// coefficients: one LDS.64 (alpha, beta) per pair instead of an LDS.128
+#define FSE_RTWIST 1
+#endif
 #ifndef FSE_PREFETCH64
 #define FSE_PREFETCH64 2  // F=64 table-load prefetch depth (4 before the FMNMX3 group step)
 #endif
@@ -898,8 +905,9 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         // an arithmetic op gives each SoA pair a fresh, aligned register
         // pair (plain copies let the allocator split the pairs and pay MOVs
         // around every FFMA2 of the hot loop)
-        Rre[p] = __fadd2_rn(make_float2(xa.x, xb.x), make_float2(0.f, 0.f));
-        Rim[p] = __fadd2_rn(make_float2(xa.y, xb.y), make_float2(0.f, 0.f));
+        const bool tw = FSE_RTWIST && ALG == 1 && F == 64 && sym;  // twisted pairs (rFSE loop)
+        Rre[p] = __fadd2_rn(make_float2(xa.x, tw ? xb.y : xb.x), make_float2(0.f, 0.f));
+        Rim[p] = __fadd2_rn(make_float2(xa.y, tw ? xb.x : xb.y), make_float2(0.f, 0.f));
       }
     }
     // e0 = sum w s^2 (slot reduction; trace energies only)
@@ -1566,6 +1574,9 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         // atom) at both atoms' shifts, the mirror atom with sg conj(c~).
         constexpr unsigned RSB = (F == 32 ? 2u : 1u) * (unsigned)G::SYM_C * 8u;  // bytes per pair step
         const unsigned crit0 = (unsigned)__cvta_generic_to_shared(region + G::TABLE_BYTES);
+        constexpr bool TW = FSE_RTWIST && F == 64;
+        // twisted layout: (alpha, beta) per (row, lane), 8 B entries
+        const unsigned rt2c = __shfl_sync(0xffffffffu, crit0 + (unsigned)(rowbase * 32 + lane) * 8u, lane);
         unsigned midx = 0;
         float c2re = 0.f, c2im = 0.f;
         int tally = 0;
@@ -1575,6 +1586,8 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           const unsigned k0 = kpos + (unsigned)(G::SYM_C - F) * (kpos >> G::LOG) + (unsigned)((F - 1) * (G::SYM_C + 1));
           const unsigned tq1 = tbase + ((k0 - gidx - (unsigned)(G::SYM_C - F) * (gidx >> G::LOG)) << 3);
           const unsigned tq2 = tbase + ((k0 - midx - (unsigned)(G::SYM_C - F) * (midx >> G::LOG)) << 3);
+          const float2 k1a = make_float2(-cre, -cim), k1b = make_float2(-cim, -cre);
+          const float2 k2a = make_float2(-c2re, -c2im), k2b = make_float2(-c2im, -c2re);
           float bst = -1.f, bxs = 0.f;
           int bps = 0;
 #pragma unroll
@@ -1582,15 +1595,28 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
             FSE_CHECK((tq1 - tbase) / 8 + (unsigned)p * (RSB / 8) < (unsigned)(G::SYM_R * G::SYM_C));
             FSE_CHECK((tq2 - tbase) / 8 + (unsigned)p * (RSB / 8) < (unsigned)(G::SYM_R * G::SYM_C));
             const float2 q1 = lds64f(tq1 + (unsigned)p * RSB), q2 = lds64f(tq2 + (unsigned)p * RSB);
-            ffma2_acc(Rre[p], q1, -cre);
-            ffma2_acc(Rim[p], q1, -cim);
-            ffma2_acc(Rre[p], q2, -c2re);
-            ffma2_acc(Rim[p], q2, -c2im);
-            const float4 ab = lds128f(rt4 + (unsigned)(p * 32 * 16));  // (alpha_a, alpha_b, beta_a, beta_b)
-            const float2 t1 = fmul2(make_float2(ab.x, ab.y), Rre[p]);
-            const float2 t2 = fmul2(make_float2(ab.z, ab.w), Rim[p]);
-            float2 cr = fmul2(t1, Rre[p]);
-            cr = ffma2(t2, Rim[p], cr);
+            float2 cr;
+            if constexpr (TW) {
+              // A = (re_a, im_b) -= (c.re, c.im) q, B = (im_a, re_b) -= (c.im, c.re) q
+              ffma2_acc2(Rre[p], q1, k1a);
+              ffma2_acc2(Rim[p], q1, k1b);
+              ffma2_acc2(Rre[p], q2, k2a);
+              ffma2_acc2(Rim[p], q2, k2b);
+              const float2 ab = lds64f(rt2c + (unsigned)(p * 32 * 8));  // (alpha, beta) of member a
+              const float2 t1 = fmul2(Rre[p], Rre[p]), t2 = fmul2(Rim[p], Rim[p]);
+              cr = fmul2(t1, make_float2(ab.x, ab.x));
+              cr = ffma2(t2, make_float2(ab.y, ab.y), cr);
+            } else {
+              ffma2_acc(Rre[p], q1, -cre);
+              ffma2_acc(Rim[p], q1, -cim);
+              ffma2_acc(Rre[p], q2, -c2re);
+              ffma2_acc(Rim[p], q2, -c2im);
+              const float4 ab = lds128f(rt4 + (unsigned)(p * 32 * 16));  // (alpha_a, alpha_b, beta_a, beta_b)
+              const float2 t1 = fmul2(make_float2(ab.x, ab.y), Rre[p]);
+              const float2 t2 = fmul2(make_float2(ab.z, ab.w), Rim[p]);
+              cr = fmul2(t1, Rre[p]);
+              cr = ffma2(t2, Rim[p], cr);
+            }
             first_max(bst, bps, bxs, cr, p);
           }
           const int myidx = bin_index<F>(w, lane, bps, bxs >= bst ? 0 : 1);
@@ -1602,6 +1628,11 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           decode_bin<F>((int)widx, w, pw, mw, ow);
           float are, aim;
           pick_bin<G::NP>(Rre, Rim, pw, mw, are, aim);
+          if (TW && mw) {  // twisted pairs hold member b as (im, re)
+            const float t = are;
+            are = aim;
+            aim = t;
+          }
           are = __shfl_sync(0xffffffffu, are, ow);
           aim = __shfl_sync(0xffffffffu, aim, ow);
           gidx = widx;
@@ -1624,9 +1655,18 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           const bool self = ((2 * u) & (F - 1)) == 0 && ((2 * v) & (F - 1)) == 0;
           const unsigned ent = F == 32 ? (u >> 1) * 32u + v : u * 32u + (v & 31u);
           const bool mb = F == 32 ? (u & 1u) != 0u : ((v >> 5) & 1u) != 0u;
-          const float4 e4 = lds128f(crit0 + ent * 16u);
+          float wal, wbe;
+          if constexpr (TW) {  // (alpha, beta) of member a; member b swaps them
+            const float2 e2 = lds64f(crit0 + ent * 8u);
+            wal = mb ? e2.y : e2.x;
+            wbe = mb ? e2.x : e2.y;
+          } else {
+            const float4 e4 = lds128f(crit0 + ent * 16u);
+            wal = mb ? e4.y : e4.x;
+            wbe = mb ? e4.w : e4.z;
+          }
           const float fac = self ? 1.f : 0.5f;
-          float pr = fac * (mb ? e4.y : e4.x) * are, pi = fac * (mb ? e4.w : e4.z) * aim;
+          float pr = fac * wal * are, pi = fac * wbe * aim;
           const float sg = ((u != 0u) != (v != 0u)) ? -1.f : 1.f;
           unsigned mi = (((F - u) & (F - 1)) << G::LOG) | ((F - v) & (F - 1));
           if (!self && mi < gidx) {  // canonical member (rfse.py:113-121)
@@ -2153,7 +2193,10 @@ __global__ void __launch_bounds__(512) class_setup_kernel(ClassSetupArgs a) {
           al[h] = flip ? y : x;
           be[h] = flip ? x : y;
         }
-        A4[i] = make_float4((float)al[0], (float)al[1], (float)be[0], (float)be[1]);
+        if (FSE_RTWIST && F == 64)  // twisted loop: member a's (alpha, beta) only
+          ((float2 *)A4)[i] = make_float2((float)al[0], (float)be[0]);
+        else
+          A4[i] = make_float4((float)al[0], (float)al[1], (float)be[0], (float)be[1]);
       }
     }
     return;
