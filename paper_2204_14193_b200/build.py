@@ -15,7 +15,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libfse_b200.so")
-SOURCES = ["csrc/generic.cu", "csrc/fast.cu", "csrc/spatial.cu", "csrc/api.cpp"]
+SOURCES = ["csrc/generic.cu", "csrc/fast.cu", "csrc/fast_small.cu", "csrc/fast_mid.cu", "csrc/spatial.cu",
+           "csrc/api.cpp"]
 DEPS = SOURCES + ["csrc/common.cuh", "csrc/dft.cuh", "csrc/kernels.h", "../include/fse_b200.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

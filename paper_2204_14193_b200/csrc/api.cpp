@@ -101,6 +101,7 @@ struct fse_plan {
   double rho = 0, gamma = 0;
   int n_classes = 0, n_rounds = 0;
   bool fast = false;
+  int variant = 0;  // fused-kernel build: 0 fast.cu, 1 fast_mid.cu (s32), 2 fast_small.cu (s16)
   bool tma_aligned = true;  // every window box starts on a 16-byte column (TMA legal)
   int max_frame = -1;       // largest frame index of the block list
   fse::FastConfig cfg{};
@@ -404,6 +405,26 @@ int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int 
   p->fast = precision == FSE_PREC_F32 &&
             fse::fast_config(F, iterations, sm_count(), &p->cfg, algorithm) &&
             B * B == 2 * (F * F / 32) && iterations > 0;
+  // Small F = 64 cFSE plans are latency-bound (each block's 100 dependent
+  // iterations, its warps alone on their SM sub-partitions): spread each
+  // block over more warps while the plan still fits one wave of the build's
+  // slots -- up to 2 blocks per SM the 8-warp build (fast_small.cu), up to
+  // 3 the 4-warp build (fast_mid.cu; measured equal at 3.5, 2 % slower at
+  // 3.5-5), beyond that the 2-warp throughput build.  All three give the
+  // same tiles and traces bit for bit.  FSE_VARIANT=0/1/2 forces one.
+  if (p->fast && F == 64 && algorithm == FSE_ALG_CFSE) {
+    const int sm = sm_count();
+    const char *venv = getenv("FSE_VARIANT");
+    int v = venv ? atoi(venv) : n_blocks <= 2 * sm ? 2 : n_blocks <= 3 * sm ? 1 : 0;
+    fse::FastConfig vc{};
+    if (v == 2 && fse::s16::fast_config(F, iterations, sm, &vc, algorithm)) {
+      p->variant = 2;
+      p->cfg = vc;
+    } else if (v == 1 && fse::s32::fast_config(F, iterations, sm, &vc, algorithm)) {
+      p->variant = 1;
+      p->cfg = vc;
+    }
+  }
   double *dmin_dev = nullptr;  // rfse.py:47-55 degeneracy check, every rFSE plan
   if (algorithm == FSE_ALG_RFSE) CK(p->alloc(&dmin_dev, (size_t)std::max(nc, 1)));
   if (p->fast) CK(p->alloc((char **)&p->table, (size_t)nc * p->cfg.table_bytes));
@@ -424,7 +445,9 @@ int fse_plan_create_ex(fse_plan **out, const int32_t *blocks, int n_blocks, int 
   ca.w64 = p->w64; ca.wtab = p->wtab; ca.fast_table = p->fast ? p->table : nullptr;
   ca.fast_table_bytes = p->fast ? p->cfg.table_bytes : 0; ca.w00 = p->w00; ca.tmp = p->tmp;
   ca.rfse = p->fast && algorithm == FSE_ALG_RFSE; ca.dmin = dmin_dev;
-  CK(fse::launch_class_setup(ca, st));
+  CK(p->variant == 2   ? fse::s16::launch_class_setup(ca, st)
+     : p->variant == 1 ? fse::s32::launch_class_setup(ca, st)
+                       : fse::launch_class_setup(ca, st));
   std::vector<double> w00(nc), dmin(nc, 1.0);
   if (nc) CK(cudaMemcpyAsync(w00.data(), p->w00, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
   if (nc && dmin_dev)
@@ -585,7 +608,10 @@ int fse_plan_run(const fse_plan *p, const void *frames, int dtype, long long pit
               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
         a.use_tma = 1;
     }
-    CK(fse::launch_fast(a, p->cfg, a.use_tma ? &tmap : nullptr, st));
+    const CUtensorMap *tm = a.use_tma ? &tmap : nullptr;
+    CK(p->variant == 2   ? fse::s16::launch_fast(a, p->cfg, tm, st)
+       : p->variant == 1 ? fse::s32::launch_fast(a, p->cfg, tm, st)
+                         : fse::launch_fast(a, p->cfg, tm, st));
     return FSE_OK;
   }
   if (trace_uv && (!trace_c || !trace_e)) return fail(FSE_ERR_VALUE, "partial trace buffers");

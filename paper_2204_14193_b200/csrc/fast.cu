@@ -37,6 +37,9 @@
 //   FSE_MAX3 / FSE_PACKKEY  alternative first-max trackers (1 / 0)
 //   FSE_DIAG                diagnostic builds (bit 32: per-phase clock probe)
 //   FSE_CHECKS              device asserts on every shared/global index
+//   FSE_FAST_NS             latency builds (fast_small.cu): this file compiled
+//                           again into fse::FSE_FAST_NS with other F=64 knobs,
+//                           F=64 cFSE only (FSE_FAST_ONLY64)
 #include <stdlib.h>
 #include <string.h>
 
@@ -47,6 +50,9 @@
 #include "kernels.h"
 
 namespace fse {
+#ifdef FSE_FAST_NS
+namespace FSE_FAST_NS {
+#endif
 
 template <int F> struct FG {
   static constexpr int LOG = F == 32 ? 5 : F == 64 ? 6 : 7;
@@ -1898,16 +1904,40 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       const float4 c4 = cq[it];
       const float2 cr = make_float2(c4.x, c4.y), ci = make_float2(c4.z, c4.w);
       const int tu = (int)(uv & 0xffffu), j0 = tu * pm + (int)(uv >> 16) * pn;
-      // twiddles of the thread's rows m0 + RS k by recurrence t_{k+1} = t_k w,
-      // w = e^{2 pi i u RS / F}: two lookups per coefficient instead of PP
-      float2 t = syn_tw[j0 & (F - 1)];
-      const float2 wv = syn_tw[(tu * RS) & (F - 1)];
-      const float2 wa = make_float2(wv.x, wv.y), wb = make_float2(-wv.y, wv.x);
+#ifndef FSE_SYN_CHAIN
+// 1 (the F=64 latency builds): follow the throughput build's twiddle chain
+// -- rows off .. off + B/2 - 1 of the pixel's column from one lookup at row
+// off, stepped by e^{2 pi i u / F} -- and accumulate the thread's own rows
+// from it, so a pixel's value is bit for bit the throughput build's whatever
+// the thread layout (results do not depend on the batch size).  0: the
+// thread's own rows m0 + RS k by the recurrence t_{k+1} = t_k e^{2 pi i u RS / F}
+#define FSE_SYN_CHAIN 0
+#endif
+      if constexpr (FSE_SYN_CHAIN && RS > 1) {
+        const int r0 = pm - off;  // the thread's first row within the chain
+        float2 t = syn_tw[(tu * off + (int)(uv >> 16) * pn) & (F - 1)];
+        const float2 wv = syn_tw[tu & (F - 1)];
+        const float2 wa = make_float2(wv.x, wv.y), wb = make_float2(-wv.y, wv.x);
 #pragma unroll
-      for (int k = 0; k < PP; ++k) {
-        g[k] = ffma2(cr, make_float2(t.x, t.x), g[k]);
-        g[k] = ffma2(ci, make_float2(t.y, t.y), g[k]);
-        if (k + 1 < PP) t = ffma2(make_float2(t.y, t.y), wb, fmul2(make_float2(t.x, t.x), wa));
+        for (int r = 0; r < G::B / 2; ++r) {
+#pragma unroll
+          for (int k = 0; k < PP; ++k)
+            if (r == r0 + RS * k) {
+              g[k] = ffma2(cr, make_float2(t.x, t.x), g[k]);
+              g[k] = ffma2(ci, make_float2(t.y, t.y), g[k]);
+            }
+          if (r + 1 < G::B / 2) t = ffma2(make_float2(t.y, t.y), wb, fmul2(make_float2(t.x, t.x), wa));
+        }
+      } else {
+        float2 t = syn_tw[j0 & (F - 1)];
+        const float2 wv = syn_tw[(tu * RS) & (F - 1)];
+        const float2 wa = make_float2(wv.x, wv.y), wb = make_float2(-wv.y, wv.x);
+#pragma unroll
+        for (int k = 0; k < PP; ++k) {
+          g[k] = ffma2(cr, make_float2(t.x, t.x), g[k]);
+          g[k] = ffma2(ci, make_float2(t.y, t.y), g[k]);
+          if (k + 1 < PP) t = ffma2(make_float2(t.y, t.y), wb, fmul2(make_float2(t.x, t.x), wa));
+        }
       }
     }
     auto store_px = [&](int q, float gk) {
@@ -1966,6 +1996,9 @@ template <int F, int ALG = 0> static size_t fast_smem(int iter_cap) {
 bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algorithm) {
   size_t smem, tb;
   int S;
+#ifdef FSE_FAST_ONLY64
+  if (F != 64 || algorithm != 0) return false;
+#endif
   if (algorithm == 1) {  // fused rFSE: F = 32, 64; F = 128 centred-frame classes only
     if (F != 32 && F != 64 && F != 128) return false;
     // (F = 128: the trace must also stay clear of the criterion table in the
@@ -2027,6 +2060,9 @@ template <int F, int ALG> static cudaError_t launch_fast_t(const FastArgs &a, co
 
 cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap,
                         cudaStream_t s) {
+#ifdef FSE_FAST_ONLY64
+  return a.F == 64 && a.algorithm == 0 ? launch_fast_t<64, 0>(a, cfg, tmap, s) : cudaErrorInvalidValue;
+#else
   if (a.algorithm == 1)
     return a.F == 64    ? launch_fast_t<64, 1>(a, cfg, tmap, s)
            : a.F == 32  ? launch_fast_t<32, 1>(a, cfg, tmap, s)
@@ -2038,6 +2074,7 @@ cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensor
     case 128: return launch_fast_t<128, 0>(a, cfg, tmap, s);
   }
   return cudaErrorInvalidValue;
+#endif
 }
 
 size_t fast_stage_bytes(int F) {
@@ -2293,4 +2330,7 @@ cudaError_t launch_class_setup(const ClassSetupArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+#ifdef FSE_FAST_NS
+}  // namespace FSE_FAST_NS
+#endif
 }  // namespace fse

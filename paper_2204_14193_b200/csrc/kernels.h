@@ -117,6 +117,18 @@ cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensor
                         cudaStream_t s);
 // staging capacity (bytes per slot) of the TMA window for window size F
 size_t fast_stage_bytes(int F);
+// latency builds of the fused kernel for small F = 64 cFSE plans
+// (fast_small.cu: 16 bins per thread; fast_mid.cu: 32 bins per thread)
+namespace s16 {
+bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algorithm = 0);
+cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap, cudaStream_t s);
+cudaError_t launch_class_setup(const ClassSetupArgs &a, cudaStream_t s);
+}  // namespace s16
+namespace s32 {
+bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algorithm = 0);
+cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap, cudaStream_t s);
+cudaError_t launch_class_setup(const ClassSetupArgs &a, cudaStream_t s);
+}  // namespace s32
 
 // ------------------------------------------------------------- image f64
 // Pack the per-window trace (us, vs int64; cs re/im f64; es f64; `counts`
