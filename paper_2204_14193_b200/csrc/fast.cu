@@ -62,7 +62,10 @@ template <int F> struct FG {
 #ifndef FSE_BPT128
 #define FSE_BPT128 64  // F=128: 256 threads per block (+4.5 % over 32)
 #endif
-  static constexpr int BPT = F == 64 ? FSE_BPT64 : F == 128 ? FSE_BPT128 : 32;  // bins per thread
+#ifndef FSE_BPT32
+#define FSE_BPT32 32  // F=32: one warp per block (16: two warps, the latency build)
+#endif
+  static constexpr int BPT = F == 64 ? FSE_BPT64 : F == 128 ? FSE_BPT128 : FSE_BPT32;  // bins per thread
   static constexpr int NP = BPT / 2;      // SoA bin pairs per thread
   static constexpr int NT = F * F / BPT;  // threads per slot
   static constexpr int NW = NT / 32;      // warps per slot
@@ -299,7 +302,7 @@ FSE_DEV float load_px(const void *frames, int dtype, size_t idx) {
 
 // row-major bin index of pair p, member mem (0 = a, 1 = b) for thread (w, lane)
 template <int F> FSE_DEV int bin_index(int w, int lane, int p, int mem) {
-  if (F == 32) return (2 * p + mem) * 32 + lane;
+  if (F == 32) return (FG<32>::RPW * w + 2 * p + mem) * 32 + lane;
   if (F == 64) return (FG<64>::RPW * w + p) * 64 + lane + 32 * mem;
   return (FG<128>::RPW * w + (p >> 1)) * 128 + lane + 64 * (p & 1) + 32 * mem;
 }
@@ -308,7 +311,7 @@ template <int F> FSE_DEV int bin_index(int w, int lane, int p, int mem) {
 template <int F> FSE_DEV void decode_bin(int idx, int w, int &p, int &mem, int &lane) {
   if (F == 32) {
     int row = idx >> 5;
-    p = row >> 1; mem = row & 1; lane = idx & 31;
+    p = (row - FG<32>::RPW * w) >> 1; mem = row & 1; lane = idx & 31;
   } else if (F == 64) {
     int row = idx >> 6;
     p = row - FG<64>::RPW * w; mem = (idx >> 5) & 1; lane = idx & 31;
@@ -1888,8 +1891,12 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     // one twiddle lookup serves both:
     //   g(m, n)       += Re{c  t},   t = e^{2 pi i (u m + v n) / F}
     //   g(m + B/2, n) += Re{c2 t},  c2 = c e^{2 pi i u (B/2) / F}.
-    constexpr int BB = G::B * G::B, SG = G::SG, GT = G::NT / SG, PP = BB / GT / 2, RS = GT / G::B;
+    // (the two-warp F=32 latency build: the first warp alone, exactly as the
+    // one-warp build, so both give the same pixels)
+    constexpr int BB = G::B * G::B, SG = G::SG,
+                  GT = G::NT / SG < BB / 2 ? G::NT / SG : BB / 2, PP = BB / GT / 2, RS = GT / G::B;
     static_assert(PP * GT * 2 == BB, "pixel pairs cover the block");
+    const bool syn = st < SG * GT;
     const int sg = st / GT, gt = st - sg * GT;
     const int pm = off + gt / G::B, pn = off + gt % G::B;
     float2 g[PP];  // (pixel (m, n), pixel (m + B/2, n)) of pair k
@@ -1899,7 +1906,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     if (false)
 #endif
 #pragma unroll 2
-    for (int it = sg; it < (ALG ? nit : a.iterations); it += SG) {
+    for (int it = sg; syn && it < (ALG ? nit : a.iterations); it += SG) {
       const unsigned uv = __float_as_uint(((const float *)sp.trace)[4 * it]);
       const float4 c4 = cq[it];
       const float2 cr = make_float2(c4.x, c4.y), ci = make_float2(c4.z, c4.w);
@@ -1966,7 +1973,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
         for (int s2 = 1; s2 < SG; ++s2) s += red[s2 * BB + q];
         store_px(q, s);
       }
-    } else {
+    } else if (syn) {
 #pragma unroll
       for (int k = 0; k < PP; ++k) {
         store_px(gt + GT * k, g[k].x);
@@ -1998,6 +2005,9 @@ bool fast_config(int F, int iterations, int sm_count, FastConfig *cfg, int algor
   int S;
 #ifdef FSE_FAST_ONLY64
   if (F != 64 || algorithm != 0) return false;
+#endif
+#ifdef FSE_FAST_ONLY32
+  if (F != 32 || algorithm != 0) return false;
 #endif
   if (algorithm == 1) {  // fused rFSE: F = 32, 64; F = 128 centred-frame classes only
     if (F != 32 && F != 64 && F != 128) return false;
@@ -2060,8 +2070,10 @@ template <int F, int ALG> static cudaError_t launch_fast_t(const FastArgs &a, co
 
 cudaError_t launch_fast(const FastArgs &a, const FastConfig &cfg, const CUtensorMap *tmap,
                         cudaStream_t s) {
-#ifdef FSE_FAST_ONLY64
+#if defined(FSE_FAST_ONLY64)
   return a.F == 64 && a.algorithm == 0 ? launch_fast_t<64, 0>(a, cfg, tmap, s) : cudaErrorInvalidValue;
+#elif defined(FSE_FAST_ONLY32)
+  return a.F == 32 && a.algorithm == 0 ? launch_fast_t<32, 0>(a, cfg, tmap, s) : cudaErrorInvalidValue;
 #else
   if (a.algorithm == 1)
     return a.F == 64    ? launch_fast_t<64, 1>(a, cfg, tmap, s)

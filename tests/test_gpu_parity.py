@@ -643,26 +643,28 @@ def test_centred_frame_and_complex_table_paths(fse, F, B, border, monkeypatch):
     assert np.median(d) < 0.5 and np.mean(d) < 0.5
 
 
-@pytest.mark.parametrize("frames_kind", ["u8", "f32"])
-def test_latency_builds_match_throughput_build(fse, frames_kind, monkeypatch):
-    """Small F = 64 cFSE plans run the 8- or 4-warp latency builds
-    (fast_small.cu / fast_mid.cu); their tiles and traces are bit for bit the
-    2-warp throughput build's (FSE_VARIANT forces each), so results do not
-    depend on the batch size."""
+@pytest.mark.parametrize("F,frames_kind", [(64, "u8"), (64, "f32")])
+def test_latency_builds_match_throughput_build(fse, F, frames_kind, monkeypatch):
+    """Small F = 64 cFSE plans run latency builds of the fused kernel (8 or 4
+    warps per block, fast_small.cu / fast_mid.cu); their tiles and traces are
+    bit for bit the throughput build's (FSE_VARIANT forces each), so results
+    do not depend on the batch size."""
     import torch
     from paper_2204_14193_b200.synth import field_torch
+    B = F // 4
     frames = field_torch(2, 540, 960, seed=41, device="cuda", edges=True)
     if frames_kind == "f32":
         frames = frames.to(torch.float32)
-    blocks = fse.frames_pattern(2, 540, 960, 16, 0.05, seed=12)
-    blocks = np.concatenate([blocks, np.array([[0, 0, 0], [1, 524, 944]], np.int32)])
+    blocks = fse.frames_pattern(2, 540, 960, B, 0.05, seed=12)
+    blocks = np.concatenate([blocks, np.array([[0, 0, 0], [1, 540 - B, 960 - B]], np.int32)])
+    want = {"0": 384, "1": 640, "2": 512}
     out = {}
-    for v in ("0", "1", "2"):
+    for v in want:
         monkeypatch.setenv("FSE_VARIANT", v)
-        plan = fse.ConcealPlan(blocks, 540, 960, iterations=100)
+        plan = fse.ConcealPlan(blocks, 540, 960, fse.Geometry(B, B, F), iterations=100)
         tiles, tr = plan.run(frames, tile_dtype="f32", trace=True)
         out[v] = (plan.info["threads"], tiles.cpu().numpy(), tr["uv"].cpu().numpy(), tr["c"].cpu().numpy())
-    assert out["0"][0] == 384 and out["1"][0] == 640 and out["2"][0] == 512, [o[0] for o in out.values()]
-    for v in ("1", "2"):
+    assert {v: o[0] for v, o in out.items()} == want
+    for v in want:
         for a, b in zip(out["0"][1:], out[v][1:]):
             assert np.array_equal(a, b), v
