@@ -29,12 +29,18 @@
 //
 // Compile-time knobs (defaults = the measured best on config 5; each was
 // A/B-measured with scripts/gpu_ab.sh, results in DESIGN.md section 4):
-//   FSE_BPT64 / FSE_BPT128  bins per thread at F=64 / 128 (64 / 64)
+//   FSE_BPT32 / FSE_BPT64 / FSE_BPT128  bins per thread (32 / 64 / 64)
 //   FSE_SLOTS64 / FSE_SLOTS32  blocks per CTA at F=64 / 32 (6 / 20)
-//   FSE_PREFETCH            W' loads issued this many pairs ahead (2)
+//   FSE_PREFETCH / FSE_PREFETCH64 / FSE_PREFETCH128  table loads issued this
+//                           many pairs ahead (2 / 2 / 0 = left to ptxas)
+//   FSE_GROUPMAX32/64/128   first-max tracked per group of bin pairs (0 / 2 / 0)
+//   FSE_GMAX3               group's last value inside the running FMNMX3 (1)
 //   FSE_CHAINS64 / FSE_CHAINS128  independent first-max chains (1 / 1)
 //   FSE_XTREE               F=128 warp-candidate merge in registers (0)
 //   FSE_MAX3 / FSE_PACKKEY  alternative first-max trackers (1 / 0)
+//   FSE_RSYM / FSE_RTWIST   centred-frame rFSE at F=32/64; F=64 twisted pairs (1 / 1)
+//   FSE_SYN_CHAIN           synthesis on the throughput build's twiddle chain
+//                           (1 in the latency builds)
 //   FSE_DIAG                diagnostic builds (bit 32: per-phase clock probe)
 //   FSE_CHECKS              device asserts on every shared/global index
 //   FSE_FAST_NS             latency builds (fast_small.cu): this file compiled
