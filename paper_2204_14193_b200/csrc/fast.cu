@@ -39,8 +39,8 @@
 //   FSE_XTREE               F=128 warp-candidate merge in registers (0)
 //   FSE_MAX3 / FSE_PACKKEY  alternative first-max trackers (1 / 0)
 //   FSE_RSYM / FSE_RTWIST   centred-frame rFSE at F=32/64; F=64 twisted pairs (1 / 1)
-//   FSE_SYN_CHAIN           synthesis on the throughput build's twiddle chain
-//                           (1 in the latency builds)
+//   FSE_SYN_GT              synthesis threads per coefficient group (0 = all;
+//                           16 in the F=64 latency builds: the throughput layout)
 //   FSE_DIAG                diagnostic builds (bit 32: per-phase clock probe)
 //   FSE_CHECKS              device asserts on every shared/global index
 //   FSE_FAST_NS             latency builds (fast_small.cu): this file compiled
@@ -1899,8 +1899,15 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     //   g(m + B/2, n) += Re{c2 t},  c2 = c e^{2 pi i u (B/2) / F}.
     // (the two-warp F=32 latency build: the first warp alone, exactly as the
     // one-warp build, so both give the same pixels)
-    constexpr int BB = G::B * G::B, SG = G::SG,
-                  GT = G::NT / SG < BB / 2 ? G::NT / SG : BB / 2, PP = BB / GT / 2, RS = GT / G::B;
+#ifndef FSE_SYN_GT
+// synthesis threads per coefficient group; the F=64 latency builds set the
+// throughput build's 16, so their synthesis runs exactly its code on the same
+// threads' worth of pixels (bit-identical tiles) while the other warps wait
+#define FSE_SYN_GT 0
+#endif
+    constexpr int GT0 = G::NT / G::SG < G::B * G::B / 2 ? G::NT / G::SG : G::B * G::B / 2;
+    constexpr int BB = G::B * G::B, SG = G::SG, GT = FSE_SYN_GT > 0 && FSE_SYN_GT < GT0 ? FSE_SYN_GT : GT0,
+                  PP = BB / GT / 2, RS = GT / G::B;
     static_assert(PP * GT * 2 == BB, "pixel pairs cover the block");
     const bool syn = st < SG * GT;
     const int sg = st / GT, gt = st - sg * GT;
@@ -1917,40 +1924,16 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       const float4 c4 = cq[it];
       const float2 cr = make_float2(c4.x, c4.y), ci = make_float2(c4.z, c4.w);
       const int tu = (int)(uv & 0xffffu), j0 = tu * pm + (int)(uv >> 16) * pn;
-#ifndef FSE_SYN_CHAIN
-// 1 (the F=64 latency builds): follow the throughput build's twiddle chain
-// -- rows off .. off + B/2 - 1 of the pixel's column from one lookup at row
-// off, stepped by e^{2 pi i u / F} -- and accumulate the thread's own rows
-// from it, so a pixel's value is bit for bit the throughput build's whatever
-// the thread layout (results do not depend on the batch size).  0: the
-// thread's own rows m0 + RS k by the recurrence t_{k+1} = t_k e^{2 pi i u RS / F}
-#define FSE_SYN_CHAIN 0
-#endif
-      if constexpr (FSE_SYN_CHAIN && RS > 1) {
-        const int r0 = pm - off;  // the thread's first row within the chain
-        float2 t = syn_tw[(tu * off + (int)(uv >> 16) * pn) & (F - 1)];
-        const float2 wv = syn_tw[tu & (F - 1)];
-        const float2 wa = make_float2(wv.x, wv.y), wb = make_float2(-wv.y, wv.x);
+      // twiddles of the thread's rows m0 + RS k by recurrence t_{k+1} = t_k w,
+      // w = e^{2 pi i u RS / F}: two lookups per coefficient instead of PP
+      float2 t = syn_tw[j0 & (F - 1)];
+      const float2 wv = syn_tw[(tu * RS) & (F - 1)];
+      const float2 wa = make_float2(wv.x, wv.y), wb = make_float2(-wv.y, wv.x);
 #pragma unroll
-        for (int r = 0; r < G::B / 2; ++r) {
-#pragma unroll
-          for (int k = 0; k < PP; ++k)
-            if (r == r0 + RS * k) {
-              g[k] = ffma2(cr, make_float2(t.x, t.x), g[k]);
-              g[k] = ffma2(ci, make_float2(t.y, t.y), g[k]);
-            }
-          if (r + 1 < G::B / 2) t = ffma2(make_float2(t.y, t.y), wb, fmul2(make_float2(t.x, t.x), wa));
-        }
-      } else {
-        float2 t = syn_tw[j0 & (F - 1)];
-        const float2 wv = syn_tw[(tu * RS) & (F - 1)];
-        const float2 wa = make_float2(wv.x, wv.y), wb = make_float2(-wv.y, wv.x);
-#pragma unroll
-        for (int k = 0; k < PP; ++k) {
-          g[k] = ffma2(cr, make_float2(t.x, t.x), g[k]);
-          g[k] = ffma2(ci, make_float2(t.y, t.y), g[k]);
-          if (k + 1 < PP) t = ffma2(make_float2(t.y, t.y), wb, fmul2(make_float2(t.x, t.x), wa));
-        }
+      for (int k = 0; k < PP; ++k) {
+        g[k] = ffma2(cr, make_float2(t.x, t.x), g[k]);
+        g[k] = ffma2(ci, make_float2(t.y, t.y), g[k]);
+        if (k + 1 < PP) t = ffma2(make_float2(t.y, t.y), wb, fmul2(make_float2(t.x, t.x), wa));
       }
     }
     auto store_px = [&](int q, float gk) {
@@ -1966,10 +1949,12 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
     };
     if constexpr (SG > 1) {
       float *red = (float *)((char *)sp.scratch + G::SCRATCH - G::SYN_RED);
+      if (syn) {
 #pragma unroll
-      for (int k = 0; k < PP; ++k) {
-        red[sg * BB + gt + GT * k] = g[k].x;
-        red[sg * BB + gt + GT * k + BB / 2] = g[k].y;
+        for (int k = 0; k < PP; ++k) {
+          red[sg * BB + gt + GT * k] = g[k].x;
+          red[sg * BB + gt + GT * k + BB / 2] = g[k].y;
+        }
       }
       slot_sync<F>(slot);
 #pragma unroll

@@ -8,5 +8,5 @@
 #define FSE_SLOTS64 5
 #define FSE_GROUPMAX64 0
 #define FSE_PREFETCH64 2
-#define FSE_SYN_CHAIN 1  // pixels bit for bit the throughput build's
+#define FSE_SYN_GT 16  // synthesis on the throughput build's thread layout: same pixels bit for bit
 #include "fast.cu"
