@@ -60,6 +60,9 @@ def parse():
                    help="where the timed step stores its tiles (host = the shared gather buffer)")
     p.add_argument("--parity-sample", type=int, default=4096,
                    help="blocks of the timed tiles checked against the CPU oracle (0 = off)")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: every rank conceals the config's full frame count (job = N x frames, "
+                        "frames r*frames .. (r+1)*frames on rank r); strong: the config's frames split over the ranks")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     return p.parse_args()
@@ -279,7 +282,7 @@ def run_reference(a, cfg, rank):
     line = {
         "impl": "reference", "metric": "lost_blocks_per_s", "value": v, "unit": "blocks/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True, "scaling": a.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config{a.config}", "frames": cfg["frames"], "H": cfg["H"],
                    "W": cfg["W"], "loss_fraction": cfg["frac"], "B": cfg["B"], "border": cfg["border"],
@@ -382,9 +385,12 @@ def main():
             red_dev = "cpu"
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    all_blocks = fse.frames_pattern(cfg["frames"], cfg["H"], cfg["W"], cfg["B"], cfg["frac"],
+    # weak scaling (default): per-GPU work fixed, the job grows with N; every
+    # frame f of the job is the same at every N (per-frame seeds)
+    job_frames = cfg["frames"] * (world if a.scaling == "weak" else 1)
+    all_blocks = fse.frames_pattern(job_frames, cfg["H"], cfg["W"], cfg["B"], cfg["frac"],
                                     SEED if a.config == "5" else 3)
-    sh = sharding.shard_blocks(all_blocks, cfg["frames"], rank, world)
+    sh = sharding.shard_blocks(all_blocks, job_frames, rank, world)
     f0, nf, blocks = sh.f0, sh.n_frames, sh.blocks
     lo, hi = sharding.contiguous_range(sh)
     frames = field_torch(nf, cfg["H"], cfg["W"], seed=frame_seed(a.config) + f0, device="cuda")
@@ -503,9 +509,9 @@ def main():
     line = {
         "metric": "lost_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"config{a.config}", "frames": cfg["frames"], "H": cfg["H"],
+        "config": {"workload": f"config{a.config}", "frames": job_frames, "frames_per_gpu": nf, "H": cfg["H"],
                    "W": cfg["W"], "loss_fraction": cfg["frac"], "blocks": total_blocks,
                    "B": cfg["B"], "border": cfg["border"], "F": F, "iterations": I, "rho": RHO,
                    "gamma": GAMMA, "seed": SEED, "parallelism": f"frames sharded x{world}",
