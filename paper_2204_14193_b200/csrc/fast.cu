@@ -960,6 +960,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       const unsigned clk0 = (unsigned)clock();
 #endif
       const int rowoff = (rowbase - (int)(gidx >> G::LOG)) & (F - 1);
+      (void)rowoff;
 #ifndef FSE_CHAINS64
 #define FSE_CHAINS64 1
 #endif
@@ -997,6 +998,8 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
       static_assert(GM == 0 || (CH == 1 && G::NP % GM == 0), "group tracker: one chain, whole groups");
       float gv[GM > 0 ? 2 * GM : 2];  // the current group's |R|^2 values
       int bg = 0;                     // GM: the thread's first group holding its maximum
+      (void)gv;
+      (void)bg;
       unsigned bkey = 0u;  // PK: truncated |R|^2 bits | (NP-1-p) << 1 | member a
       // (the mask laundered through a shuffle stays a register operand, so
       // clear-and-insert is one LOP3 with the rank as its immediate)
@@ -1044,6 +1047,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           float2 mg = fmul2(Rre[p], Rre[p]);
           mg = ffma2(Rim[p], Rim[p], mg);
           const int ch = p / (G::NP / CH);
+          (void)ch;
 #if FSE_DIAG & 2
           bst[ch] = fmax3(bst[ch], mg.x, mg.y);
 #else
@@ -1094,6 +1098,7 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           float2 mg = fmul2(Rre[p], Rre[p]);
           mg = ffma2(Rim[p], Rim[p], mg);
           const int ch = p / (G::NP / CH);
+          (void)ch;
 #if FSE_DIAG & 2
           bst[ch] = fmax3(bst[ch], mg.x, mg.y);
 #else
@@ -1144,8 +1149,9 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           const int q = p & 1;
           float2 qv;
           if constexpr (PQ > 0) {
-            qv = qb[p % PQ];
-            if (p + PQ < G::NP) qb[p % PQ] = ldq(p + PQ);
+            constexpr int PQ1 = PQ > 0 ? PQ : 1;
+            qv = qb[p % PQ1];
+            if (p + PQ < G::NP) qb[p % PQ1] = ldq(p + PQ);
           } else {
             qv = ldq(p);
           }
