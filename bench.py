@@ -68,6 +68,12 @@ def parse():
     return p.parse_args()
 
 
+def job_frames(frames: int, world: int, scaling: str) -> int:
+    """Frames of the whole job: weak scaling keeps `frames` per rank (the job
+    grows with N), strong scaling splits `frames` over the ranks."""
+    return frames * (world if scaling == "weak" else 1)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -387,10 +393,10 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # weak scaling (default): per-GPU work fixed, the job grows with N; every
     # frame f of the job is the same at every N (per-frame seeds)
-    job_frames = cfg["frames"] * (world if a.scaling == "weak" else 1)
-    all_blocks = fse.frames_pattern(job_frames, cfg["H"], cfg["W"], cfg["B"], cfg["frac"],
+    n_job = job_frames(cfg["frames"], world, a.scaling)
+    all_blocks = fse.frames_pattern(n_job, cfg["H"], cfg["W"], cfg["B"], cfg["frac"],
                                     SEED if a.config == "5" else 3)
-    sh = sharding.shard_blocks(all_blocks, job_frames, rank, world)
+    sh = sharding.shard_blocks(all_blocks, n_job, rank, world)
     f0, nf, blocks = sh.f0, sh.n_frames, sh.blocks
     lo, hi = sharding.contiguous_range(sh)
     frames = field_torch(nf, cfg["H"], cfg["W"], seed=frame_seed(a.config) + f0, device="cuda")
@@ -511,7 +517,7 @@ def main():
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"config{a.config}", "frames": job_frames, "frames_per_gpu": nf, "H": cfg["H"],
+        "config": {"workload": f"config{a.config}", "frames": n_job, "frames_per_gpu": nf, "H": cfg["H"],
                    "W": cfg["W"], "loss_fraction": cfg["frac"], "blocks": total_blocks,
                    "B": cfg["B"], "border": cfg["border"], "F": F, "iterations": I, "rho": RHO,
                    "gamma": GAMMA, "seed": SEED, "parallelism": f"frames sharded x{world}",

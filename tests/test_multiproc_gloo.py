@@ -90,3 +90,29 @@ def test_shard_blocks_rebases_frames():
     assert np.array_equal(s.blocks, [[0, 32, 0], [1, 0, 48]])
     with pytest.raises(ValueError):
         sharding.assemble([np.zeros((1, 2, 2))], [np.array([0])], 2)
+
+
+def test_weak_scaling_shards_keep_the_n1_share():
+    """bench.py's default (weak scaling): rank r of N conceals frames
+    256 r .. 256 r + 255 of an N x 256-frame job, and every frame's loss
+    pattern is the same at every N (per-frame seeds)."""
+    import importlib.util
+    import os as _os
+
+    import paper_2204_14193_b200 as fse
+
+    spec = importlib.util.spec_from_file_location(
+        "bench", _os.path.join(_os.path.dirname(_os.path.dirname(__file__)), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    per, H, W = 3, 270, 480
+    base = fse.frames_pattern(per, H, W, 16, 0.05, seed=5)
+    for world in [1, 2, 4, 8]:
+        n = bench.job_frames(per, world, "weak")
+        assert n == per * world and bench.job_frames(per, world, "strong") == per
+        job = fse.frames_pattern(n, H, W, 16, 0.05, seed=5)
+        assert np.array_equal(job[job[:, 0] < per], base)
+        for r in range(world):
+            sh = sharding.shard_blocks(job, n, r, world)
+            assert (sh.f0, sh.n_frames) == (per * r, per)
+            assert np.array_equal(sh.blocks[:, 0], job[job[:, 0] // per == r][:, 0] - per * r)
