@@ -28,13 +28,10 @@ import paper_2204_14193_b200 as fse  # noqa: E402
 from paper_2204_14193_b200.synth import field_torch  # noqa: E402
 
 
-def main():
-    p = argparse.ArgumentParser()
-    p.add_argument("--config", default="5", choices=sorted(bench.CONFIGS))
-    p.add_argument("--chunk", type=int, default=32)
-    p.add_argument("--frames", type=int, default=None)
-    p.add_argument("--out", default=None)
-    a = p.parse_args()
+def run(config: str = "5", chunk: int = 32, n_frames: int | None = None, verbose: bool = False):
+    """Gate every lost block of bench.py's workload `config`; returns
+    (summary record, per-chunk records)."""
+    a = argparse.Namespace(config=config, chunk=chunk, frames=n_frames)
     cfg = dict(bench.CONFIGS[a.config])
     if a.frames:
         cfg["frames"] = a.frames
@@ -66,7 +63,8 @@ def main():
         for k in ("over_0p5", "certified_strict", "certified_bounded"):
             tot[k] += r[k] or 0
         tot["max_dev"] = max(tot["max_dev"], r["max_dev"] or 0.0)
-        print(json.dumps(r), flush=True)
+        if verbose:
+            print(json.dumps(r), flush=True)
     rec = {"workload": f"config{a.config}", "frames": nf, "H": cfg["H"], "W": cfg["W"],
            "iterations": cfg["iters"], "F": cfg["F"], **tot,
            "psnr_delta_db_worst_chunk": max((abs(c["psnr_delta_db"]) for c in chunks
@@ -74,6 +72,17 @@ def main():
            "timed_u8_equal_every_chunk": all(c["timed_u8_equal"] for c in chunks),
            "passed": bool(ok and tot["blocks"] == len(blocks)), "seconds": round(time.time() - t0, 1),
            "gate": chunks[0]["gate"] if chunks else None}
+    return rec, chunks
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", default="5", choices=sorted(bench.CONFIGS))
+    p.add_argument("--chunk", type=int, default=32)
+    p.add_argument("--frames", type=int, default=None)
+    p.add_argument("--out", default=None)
+    a = p.parse_args()
+    rec, chunks = run(a.config, a.chunk, a.frames, verbose=True)
     print(json.dumps(rec))
     if a.out:
         with open(a.out, "w") as f:

@@ -263,6 +263,29 @@ def test_config5_fp32(fse, gen):
     print("config5", gen, {k: v for k, v in st.items() if k != "outliers"})
 
 
+@pytest.mark.slow
+def test_config5_every_block_fp32(fse):
+    """The whole benched workload: all 256 frames of config 5 as bench.py
+    generates them, every one of the 414,720 lost blocks.  The u8 tiles of
+    one full plan run (what the bench times) must equal the 32-frame chunked
+    f32 re-runs bit for bit, and every chunk passes bench.py's oracle gate
+    (per block <= 0.5 gray levels except certified near-ties, pooled PSNR
+    within 0.01 dB).  About a minute on the GPU box's host threads
+    (scripts/config5_full_parity.py; record in profiles/r02)."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                        "config5_full_parity.py")
+    spec = importlib.util.spec_from_file_location("config5_full_parity", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    rec, chunks = mod.run("5")
+    print("config5 every block", rec)
+    assert rec["blocks"] == 414720 and rec["timed_u8_equal_every_chunk"]
+    bad = [c for c in chunks if not c["passed"]]
+    assert rec["passed"] and not bad, bad[:2]
+
+
 def test_fp64_plan_matches_oracle(fse):
     """fp64 image-level path (config 1 + clipped blocks): tiles within 1e-9."""
     from paper_2204_14193_b200.synth import field
