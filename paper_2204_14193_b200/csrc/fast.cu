@@ -35,6 +35,7 @@
 //                           many pairs ahead (2 / 2 / 0 = left to ptxas)
 //   FSE_GROUPMAX32/64/128   first-max tracked per group of bin pairs (0 / 2 / 0)
 //   FSE_GMAX3               group's last value inside the running FMNMX3 (1)
+//   FSE_RESOLVE_SEL / FSE_IDXSHFL  F=64 tail: select-tree group resolution, whole-index shuffle (1 / 1)
 //   FSE_CHAINS64 / FSE_CHAINS128  independent first-max chains (1 / 1)
 //   FSE_XTREE               F=128 warp-candidate merge in registers (0)
 //   FSE_MAX3 / FSE_PACKKEY  alternative first-max trackers (1 / 0)
@@ -484,6 +485,26 @@ FSE_DEV void resolve_group(const float2 (&Rre)[NP], const float2 (&Rim)[NP], int
       FSE_RG(8) FSE_RG(9) FSE_RG(10) FSE_RG(11) FSE_RG(12) FSE_RG(13) FSE_RG(14) FSE_RG(15)
       default: __builtin_unreachable();
     }
+  }
+#ifndef FSE_RESOLVE_SEL
+// 1: GM = 2 resolution as a two-level select tree instead of four overwrite passes (14 ops
+// for 26 on the per-iteration serial tail; config 5: 8.37 -> 8.59 M blocks/s, bitwise identical)
+#define FSE_RESOLVE_SEL 1
+#endif
+  if constexpr (FSE_RESOLVE_SEL && GM == 2) {
+    // the caller's lane holds target in this group, so the fourth value needs no test
+    const float2 m0 = __ffma2_rn(gi[0], gi[0], __fmul2_rn(gr[0], gr[0]));
+    const float2 m1 = __ffma2_rn(gi[1], gi[1], __fmul2_rn(gr[1], gr[1]));
+    const bool e0 = m0.x == target, e1 = m0.y == target, e2 = m1.x == target;
+    const bool lo = e0 || e1;
+    const float ra = e0 ? gr[0].x : gr[0].y, rb = e2 ? gr[1].x : gr[1].y;
+    const float ia = e0 ? gi[0].x : gi[0].y, ib = e2 ? gi[1].x : gi[1].y;
+    re = lo ? ra : rb;
+    im = lo ? ia : ib;
+    const int k = lo ? (e0 ? 0 : 1) : (e2 ? 2 : 3);
+    pp = g * GM + (k >> 1);
+    mm = k & 1;
+    return;
   }
   // scan backwards so the first match in (pair, member) order is kept
   pp = g * GM;
@@ -1228,8 +1249,19 @@ __global__ void __launch_bounds__(KS<F, ALG>::CTA, 1)
           int pp, mm;
           float re = 0.f, im = 0.f;
           resolve_group<G::NP, GM>(Rre, Rim, gL, wbest, pp, mm, re, im);
-          const int pm = __shfl_sync(0xffffffffu, (pp << 1) | mm, L);
-          const unsigned idx = (unsigned)bin_index<F>(w, L, pm >> 1, pm & 1);
+#ifndef FSE_IDXSHFL
+// 1 (F = 64): the candidate lane's bin index is shuffled whole instead of rebuilt from
+// (warp, lane, pair, member): no S2R of the thread index on the tail (8.59 -> 8.78 M)
+#define FSE_IDXSHFL 1
+#endif
+          unsigned idx;
+          if constexpr (FSE_IDXSHFL && F == 64 && !G::PLANAR) {
+            // F = 64: bin (pair p, member m) of a thread is kpos + 64 p + 32 m = kpos + 32 (2 p + m)
+            idx = __shfl_sync(0xffffffffu, kpos + ((unsigned)((pp << 1) | mm) << 5), L);
+          } else {
+            const int pm = __shfl_sync(0xffffffffu, (pp << 1) | mm, L);
+            idx = (unsigned)bin_index<F>(w, L, pm >> 1, pm & 1);
+          }
           re = __shfl_sync(0xffffffffu, re, L);
           im = __shfl_sync(0xffffffffu, im, L);
           if (idx < widx) { widx = idx; are = re; aim = im; }
